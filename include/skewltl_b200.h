@@ -1,0 +1,121 @@
+/*
+ * skewltl_b200 — C ABI of the B200 (sm_100a) pivoted LTL^T hot path.
+ *
+ * Drop-in boundary for the reference `skewltl` package (arXiv 2411.09859
+ * artefact).  The reference is pure Python (numpy/OpenBLAS); each entry point
+ * below replaces the reference function named in its comment, with the same
+ * argument meaning, in-place/ownership rules and error behaviour, expressed
+ * as plain pointers and sizes.  The Python mirror package
+ * `paper_2411_09859_b200` binds these with ctypes.
+ *
+ * Conventions
+ *   - every matrix pointer is DEVICE memory, column-major, with explicit ld;
+ *     skew matrices are stored as their strictly-lower triangle, entries on or
+ *     above the diagonal are never read (and never written except where a
+ *     function says it copies them);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream); no
+ *     function synchronises the stream;
+ *   - device scalars/arrays documented as such are written asynchronously;
+ *   - return value: skl_status; on SKL_CUDA_ERROR skl_last_error() describes it.
+ */
+#ifndef SKEWLTL_B200_H
+#define SKEWLTL_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SKL_OK = 0,
+  SKL_ZERO_PIVOT = 1,  /* unpivoted breakdown; column in *info (core.py:17-22 ZeroPivot) */
+  SKL_BAD_ARGUMENT = 2, /* dimension / ld / block mismatch (ValueError) */
+  SKL_ALIAS = 3,        /* output aliases an operand (kernels3.py:64-66) */
+  SKL_CUDA_ERROR = 4,
+  SKL_UNSUPPORTED = 5,  /* e.g. variant name (InvalidVariant, blocked.py:314-315) */
+  SKL_BAD_PIVOT = 6     /* pivot index out of range (IndexError, core.py:306-307) */
+} skl_status;
+
+/* trailing-update scheme of the pivoted blocked driver (blocked.py:35) */
+enum { SKL_VAR1 = 0, SKL_VAR2A = 1, SKL_VAR2B = 2 };
+enum { SKL_F64 = 0, SKL_F32 = 1 };
+
+const char* skl_version(void);
+const char* skl_last_error(void);
+
+/* ---- level-3: trailing sandwiched updates --------------------------------
+ * skew_rank2k (kernels3.py:305-351):
+ *   C_lower := beta*C + alpha*(A B^T - B A^T); A, B are n x k; with
+ *   skip_zero_cols, columns zero in A or in B are dropped (keff <= k).
+ *   *keff_dev (device int, may be NULL) receives keff.                     */
+size_t skl_skr2k_workspace_size(int n, int k);
+int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, const double* B, long long ldb,
+                    double beta, double* C, long long ldc, int skip_zero_cols, void* workspace,
+                    size_t workspace_bytes, int* keff_dev, void* stream);
+
+/* skew_tridiag_rankk (kernels3.py:151-209):
+ *   C_lower := beta*C + alpha * A T A^T, T = tridiag(tau[0..k-2]) skew.     */
+size_t skl_sktri_rankk_workspace_size(int n, int k);
+int skl_sktri_rankk_lower(int n, int k, double alpha, const double* A, long long lda, const double* tau,
+                          double beta, double* C, long long ldc, void* workspace, size_t workspace_bytes,
+                          void* stream);
+
+/* form_w + form_s_splitting (kernels3.py:354-364, core.py:153-169):
+ *   W = A S with T = S - S^T, tau of length k-1; even columns of W are 0.   */
+int skl_form_w(int n, int k, const double* A, long long lda, const double* tau, double* W, long long ldw,
+               void* stream);
+
+/* ---- level-2 --------------------------------------------------------------
+ * skew_rank2 (kernels2.py:93-131): A_lower := beta*A + alpha*(x y^T - y x^T) */
+int skl_skew_rank2_lower(int n, double alpha, const double* x, const double* y, double beta, double* A,
+                         long long lda, void* stream);
+
+/* skew_tridiag_gemv (kernels2.py:178-229):
+ *   y := beta*y + alpha*(A (T x))[tail_from:], A is p x k, T = tridiag(tau[0..k-2]) */
+int skl_skew_tridiag_gemv(int p, int k, double alpha, const double* A, long long lda, const double* tau,
+                          const double* x, double beta, double* y, int tail_from, void* stream);
+
+/* apply_row_pivots (kernels2.py:232-271): rows [lo, hi) of the n x q block
+ *   := rows idx[lo..hi) (idx: device int64 gather index of length n, composed
+ *   on the host from the pivot vector exactly as the reference does).       */
+size_t skl_apply_row_pivots_workspace_size(int q, int lo, int hi);
+int skl_apply_row_pivots(int n, int q, double* block, long long ld, const long long* idx, int lo, int hi,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* apply_symmetric_pivot (core.py:327-333): X := P X P^T, P = (k, k+pi).     */
+int skl_apply_symmetric_pivot(int n, double* X, long long ld, int k, long long pi, void* stream);
+
+/* ---- factorization drivers -------------------------------------------------
+ * ltlt_blk_piv (blocked.py:303-363): pivoted blocked right-looking LTL^T.
+ *   X (n x n, lower read) is not modified.  L (n x n) receives the work
+ *   buffer of the reference: L column j (j>=1) in column j-1 below the
+ *   diagonal with an explicit 1 at [j, j-1] (UnitLowerFactor "ones",
+ *   core.py:172-186); if L != X its upper triangle and diagonal are copied
+ *   from X.  tau (n-1) and piv (n, int64 relative offsets, piv[0] = 0) are
+ *   device outputs.  variant: SKL_VAR1 / SKL_VAR2A / SKL_VAR2B.             */
+size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant);
+int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
+                     double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ltlt_unb_twostep (unblocked.py:229-240): Wimmer two-step, optional pivoting.
+ *   Same output layout.  Unpivoted breakdown: *info_dev (device int) is set
+ *   to the column + 1 (0 = success) — ZeroPivot(column) on the host.        */
+size_t skl_ltlt_unb_twostep_workspace_size(int n);
+int skl_ltlt_unb_twostep(int n, int pivot, const double* X, long long ldx, double* L, long long ldl, double* tau,
+                         long long* piv, int* info_dev, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Batched pivoted factorization + Pfaffian (pfaffian, apps.py:12-30, applied
+ * to `batch` independent matrices).  dtype SKL_F64 or SKL_F32 selects the
+ * element type of X, L and tau.  Matrix b lives at X + b*strideX (elements).
+ * pf_sign/pf_logabs (device doubles, may be NULL) receive sign(Pf) and
+ * log|Pf| (overflow-free form of apps.py:26-30).                            */
+int skl_ltlt_batched_piv(int batch, int n, int dtype, const void* X, long long ldx, long long strideX, void* L,
+                         long long ldl, long long strideL, void* tau, long long* piv, double* pf_sign,
+                         double* pf_logabs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKEWLTL_B200_H */

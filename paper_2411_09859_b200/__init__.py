@@ -1,0 +1,15 @@
+"""paper_2411_09859_b200: B200-native pivoted LTL^T of skew-symmetric matrices.
+
+Drop-in for the reference ``skewltl`` hot path (arXiv 2411.09859): the same
+public names and result types, computed by hand-written sm_100a CUDA kernels
+behind the C ABI in ``include/skewltl_b200.h``.  There is no CPU fallback.
+"""
+
+from .core import (InvalidVariant, PermutationVector, PivotUnsupported, SingularT,  # noqa: F401
+                   SkewMatrixLower, SkewTridiagonal, SSplitting, UnitLowerFactor, ZeroPivot,
+                   compose_permutation, form_s_splitting, invert_permutation, random_skew)
+from .instrument import FlopCounter  # noqa: F401
+from .blocked import (DEFAULT_BLOCK, FactorizationResult, Features, ltlt_blk_piv,  # noqa: F401
+                      ltlt_blk_piv_device)
+
+__version__ = "0.1.0"

@@ -1,0 +1,121 @@
+"""Pivoted blocked LTL^T on the B200 (drop-in for reference ``blocked.py``).
+
+``ltlt_blk_piv`` keeps the reference signature (blocked.py:303-363) and
+returns the same ``FactorizationResult`` (L in the "ones" working layout,
+tau, relative pivot offsets, flop tally).  The computation is entirely the
+CUDA library's ``skl_ltlt_blk_piv``: pivoted left-looking panel kernel,
+packed operand formation and the lower-triangular DMMA trailing GEMM.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _capi
+from . import device as dv
+from .core import (InvalidVariant, PermutationVector, SkewMatrixLower, SkewTridiagonal,
+                   UnitLowerFactor)
+from .instrument import FlopCounter, flops_blk_piv
+
+DEFAULT_BLOCK = 256                               # blocked.py:34
+PIVOTED_FUSED = ("var1", "var2a", "var2b")       # blocked.py:35
+
+
+@dataclass
+class Features:
+    """Accepted for signature compatibility (blocked.py:38-62); GPU tiling is
+    internal, so the CPU optimisation-ladder toggles have no effect."""
+
+    fused_l2: bool = True
+    parallel_l2: bool = False
+    external_t: bool = True
+    fused_l3: bool = True
+
+
+@dataclass
+class FactorizationResult:
+    """L, T, pivots and the flop tally of one factorization (unblocked.py:30-40)."""
+
+    l: UnitLowerFactor
+    t: SkewTridiagonal
+    p: PermutationVector
+    flops: FlopCounter
+
+
+def _check_block(b):
+    if b < 1:
+        raise ValueError("block size must be >= 1")
+
+
+def ltlt_blk_piv_device(x, b=DEFAULT_BLOCK, fused="var1", out=None, stream=None):
+    """Device-resident entry: ``x`` is a column-major float64 CUDA tensor.
+
+    Returns ``(L, tau, piv)`` CUDA tensors without synchronising.  ``out``
+    may supply preallocated ``(L, tau, piv)`` (L may be ``x`` itself for an
+    in-place factorization).
+    """
+    if fused not in PIVOTED_FUSED:
+        raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
+    _check_block(b)
+    t = dv.require_cuda()
+    if not dv.is_colmajor_cuda(x) or x.dtype != t.float64:
+        raise ValueError("x must be a column-major float64 CUDA tensor")
+    m = x.shape[0]
+    if m < 1:
+        raise ValueError("m >= 1 required")
+    if out is None:
+        L = dv.empty_colmajor(m, m, t.float64)
+        tau = t.empty(max(m - 1, 0), dtype=t.float64, device=x.device)
+        piv = t.empty(m, dtype=t.int64, device=x.device)
+    else:
+        L, tau, piv = out
+    lib = _capi.load()
+    code = _capi.VARIANT_CODES[fused]
+    nbytes = lib.skl_ltlt_blk_piv_workspace_size(m, int(b), code)
+    if nbytes == 0:
+        raise InvalidVariant("configuration not supported by the GPU panel kernel")
+    ws = dv.workspace(nbytes)
+    st = lib.skl_ltlt_blk_piv(m, int(b), code, x.data_ptr(), dv.ld_of(x), L.data_ptr(), dv.ld_of(L),
+                              tau.data_ptr() if m > 1 else None, piv.data_ptr(), ws.data_ptr(), nbytes,
+                              dv.stream_ptr(stream))
+    _capi.check(st, "ltlt_blk_piv")
+    return L, tau, piv
+
+
+def ltlt_blk_piv(x: SkewMatrixLower, b=DEFAULT_BLOCK, fused="var1", features=None) -> FactorizationResult:
+    """Pivoted blocked right-looking factorization (blocked.py:303-363).
+
+    The input is never mutated.  NumPy input returns NumPy factors (drop-in);
+    a torch CUDA ``data`` buffer returns device-resident L and tau.
+    """
+    if fused not in PIVOTED_FUSED:
+        raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
+    _check_block(b)
+    if not isinstance(x, SkewMatrixLower):
+        x = SkewMatrixLower(x)
+    m = x.m
+    if m < 1:
+        raise ValueError("m >= 1 required")
+    on_device = dv.is_colmajor_cuda(x.data)
+    if on_device:
+        xd = x.data
+        if xd.dtype != dv.torch().float64:
+            raise TypeError("the blocked GPU path computes in float64")
+    else:
+        host = np.asarray(x.data)
+        if host.dtype == object:
+            raise TypeError("exact (object) dtypes are served by the reference, not the GPU path")
+        if host.dtype != np.float64:
+            raise TypeError("the blocked GPU path computes in float64")
+        xd = dv.to_device_colmajor(host)
+    L, tau, piv = ltlt_blk_piv_device(xd, b, fused)
+    piv_h = piv.cpu().numpy()
+    tau_h = tau.cpu().numpy()
+    flops = flops_blk_piv(m, b, fused, piv_h, tau_h)
+    if on_device:
+        return FactorizationResult(UnitLowerFactor(L, "ones"), SkewTridiagonal(tau), PermutationVector(piv_h, m),
+                                   flops)
+    return FactorizationResult(UnitLowerFactor(dv.to_host_colmajor(L), "ones"), SkewTridiagonal(tau_h),
+                               PermutationVector(piv_h, m), flops)

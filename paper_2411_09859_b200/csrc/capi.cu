@@ -1,0 +1,424 @@
+// extern "C" boundary and the host-side blocked driver.
+//
+// The driver is the B200 counterpart of ltlt_blk_piv (blocked.py:303-363):
+// per panel it launches (1) the cooperative pivoted panel kernel, (2) the
+// operand pack (B = A T^T on the fly, plus the var1 straggler pair), and
+// (3) the lower-triangular DMMA GEMM on the trailing matrix; after the last
+// panel, one gather applies the deferred row interchanges to the L columns.
+// Everything is enqueued on the caller's stream with no host synchronisation.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "skewltl_b200.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail_cuda(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return SKL_CUDA_ERROR;
+}
+
+#define SKL_TRY(expr)                                  \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return fail_cuda(_e, #expr); \
+  } while (0)
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// simple bump allocator over a caller-provided workspace (or a size query)
+struct Bump {
+  unsigned char* base;
+  size_t off = 0;
+  explicit Bump(void* b) : base(static_cast<unsigned char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    size_t o = align_up(off);
+    off = o + count * sizeof(T);
+    return base ? reinterpret_cast<T*>(base + o) : nullptr;
+  }
+};
+
+bool overlaps(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  auto pa = reinterpret_cast<uintptr_t>(a), pb = reinterpret_cast<uintptr_t>(b);
+  return pa < pb + bbytes && pb < pa + abytes;
+}
+
+size_t mat_bytes(int rows, int cols, long long ld) {
+  if (rows <= 0 || cols <= 0) return 0;
+  return ((size_t)(cols - 1) * ld + rows) * sizeof(double);
+}
+
+// ---------------------------------------------------------------------------
+// panel schedule of the pivoted blocked driver (blocked.py:325-362), with the
+// panel width shrunk when the panel block would not fit in shared memory
+// ---------------------------------------------------------------------------
+struct PanelPlan {
+  int r, nelim, lo;
+  int ctas, rows_per, kmax;
+};
+
+size_t smem_limit() {
+  static int lim = 0;
+  if (!lim) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || lim <= 0)
+      lim = 232448;
+  }
+  return (size_t)lim;
+}
+
+bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
+  int rows = n - (lo + 1);
+  int ctas = (rows + 7) / 8;
+  if (ctas > nsm) ctas = nsm;
+  if (ctas < 1) ctas = 1;
+  int R = (rows + ctas - 1) / ctas;
+  if (R > 2 * skl::panel_threads()) return false;
+  int nelim = want;
+  while (nelim >= 1 && skl::panel_smem_bytes(R, r + nelim - lo) > smem_limit()) --nelim;
+  if (nelim < 1) return false;
+  p = PanelPlan{r, nelim, lo, ctas, R, r + nelim - lo};
+  return true;
+}
+
+bool make_schedule(int n, int nb, int variant, std::vector<PanelPlan>& out) {
+  out.clear();
+  int nsm = skl::panel_max_ctas();
+  PanelPlan p;
+  if (variant == SKL_VAR2B) {
+    int done = 0;
+    bool first = true;
+    while (done < n - 1) {
+      int want = std::min(nb + (first ? 1 : 0), n - 1 - done);
+      int lo = first ? 0 : done - 1;
+      if (!plan_panel(n, done, want, lo, nsm, p)) return false;
+      out.push_back(p);
+      done += p.nelim;
+      first = false;
+    }
+  } else {
+    int r = 0;
+    bool pending = false;
+    while (r < n - 1) {
+      int want = std::min(nb, n - 1 - r);
+      int lo = (variant == SKL_VAR2A && pending) ? r - 1 : r;
+      if (!plan_panel(n, r, want, lo, nsm, p)) return false;
+      out.push_back(p);
+      r += p.nelim;
+      pending = true;
+    }
+  }
+  return true;
+}
+
+struct BlkWorkspace {
+  double* W;
+  double* P;
+  double* Q;
+  double* side;
+  double* y;
+  int* gperm_all;
+  int* sigma_all;
+  int* col_group;
+  int* disp_list;
+  int* disp_count;
+  uint64_t* slots;
+  uint64_t* rowa;
+  size_t ll_bytes;
+  int k4cap, slot_words, np;
+};
+
+size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base, BlkWorkspace* ws) {
+  Bump b(base);
+  int kmax = 1, nelim_max = 1, ctas = 1;
+  for (auto& p : plan) {
+    kmax = std::max(kmax, p.kmax);
+    nelim_max = std::max(nelim_max, p.nelim);
+    ctas = std::max(ctas, p.ctas);
+  }
+  (void)nb;
+  int np = (int)plan.size();
+  int k4cap = (kmax + 2 + 3) / 4;
+  int slot_words = 4 + 2 * (kmax + 2);
+  BlkWorkspace w{};
+  w.W = b.take<double>((size_t)n * n);
+  w.P = b.take<double>(skl::packed_elems(n, k4cap));
+  w.Q = b.take<double>(skl::packed_elems(n, k4cap));
+  w.side = b.take<double>((size_t)2 * (nelim_max + 1) * n);
+  w.y = b.take<double>(n);
+  w.gperm_all = b.take<int>((size_t)std::max(np, 1) * n);
+  w.sigma_all = b.take<int>((size_t)std::max(np, 1) * n);
+  w.col_group = b.take<int>(n);
+  w.disp_list = b.take<int>(2 * (nelim_max + 1));
+  w.disp_count = b.take<int>(1);
+  size_t ll_start = align_up(b.off);
+  w.slots = b.take<uint64_t>((size_t)ctas * 2 * slot_words);
+  w.rowa = b.take<uint64_t>((size_t)2 * slot_words);
+  w.ll_bytes = b.off - ll_start;
+  w.k4cap = k4cap;
+  w.slot_words = slot_words;
+  w.np = np;
+  if (ws) *ws = w;
+  return b.off + 256;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* skl_version(void) { return "skewltl_b200 0.1.0 (sm_100a)"; }
+const char* skl_last_error(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------
+size_t skl_skr2k_workspace_size(int n, int k) {
+  Bump b(nullptr);
+  int k4cap = (2 * std::max(k, 1) + 3) / 4;
+  b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
+  b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
+  b.take<int>(std::max(k, 1));
+  b.take<int>(4);
+  return b.off + 256;
+}
+
+int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, const double* B, long long ldb,
+                    double beta, double* C, long long ldc, int skip_zero_cols, void* workspace,
+                    size_t workspace_bytes, int* keff_dev, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n < 0 || k < 0 || (n > 0 && (lda < n || ldb < n || ldc < n))) return SKL_BAD_ARGUMENT;
+  if (workspace_bytes < skl_skr2k_workspace_size(n, k)) return SKL_BAD_ARGUMENT;
+  size_t cb = mat_bytes(n, n, ldc);
+  if (overlaps(C, cb, A, mat_bytes(n, k, lda)) && k > 0) return SKL_ALIAS;
+  if (overlaps(C, cb, B, mat_bytes(n, k, ldb)) && k > 0) return SKL_ALIAS;
+  Bump b(workspace);
+  int k4cap = (2 * std::max(k, 1) + 3) / 4;
+  double* P = b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
+  double* Q = b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
+  int* keep = b.take<int>(std::max(k, 1));
+  int* cnt = b.take<int>(4);  // [0] keff, [1] nk4
+  if (n <= 1) {
+    if (keff_dev) SKL_TRY(cudaMemsetAsync(keff_dev, 0, sizeof(int), st));
+    return SKL_OK;
+  }
+  if (k == 0 || alpha == 0.0) {
+    SKL_TRY(skl::launch_scale_lower<double>(C, ldc, n, beta, st));
+    if (keff_dev) {
+      if (k == 0) {
+        SKL_TRY(cudaMemsetAsync(keff_dev, 0, sizeof(int), st));
+      } else {
+        SKL_TRY(skl::launch_rank2k_keep(A, lda, B, ldb, n, k, skip_zero_cols, keep, cnt, cnt + 1, st));
+        SKL_TRY(cudaMemcpyAsync(keff_dev, cnt, sizeof(int), cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    return SKL_OK;
+  }
+  SKL_TRY(skl::launch_rank2k_keep(A, lda, B, ldb, n, k, skip_zero_cols, keep, cnt, cnt + 1, st));
+  SKL_TRY(skl::launch_pack_rank2k(A, lda, B, ldb, n, k, alpha, keep, cnt, k4cap, P, Q, st));
+  SKL_TRY(skl::launch_gemm_lower(P, Q, k4cap, k4cap, cnt + 1, C, ldc, n, beta, st));
+  if (keff_dev) SKL_TRY(cudaMemcpyAsync(keff_dev, cnt, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return SKL_OK;
+}
+
+size_t skl_sktri_rankk_workspace_size(int n, int k) {
+  Bump b(nullptr);
+  int k4cap = (std::max(k, 1) + 3) / 4;
+  b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
+  b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
+  return b.off + 256;
+}
+
+int skl_sktri_rankk_lower(int n, int k, double alpha, const double* A, long long lda, const double* tau,
+                          double beta, double* C, long long ldc, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n < 0 || k < 0 || (n > 0 && (lda < n || ldc < n))) return SKL_BAD_ARGUMENT;
+  if (workspace_bytes < skl_sktri_rankk_workspace_size(n, k)) return SKL_BAD_ARGUMENT;
+  if (k > 0 && overlaps(C, mat_bytes(n, n, ldc), A, mat_bytes(n, k, lda))) return SKL_ALIAS;
+  if (n <= 1) return SKL_OK;
+  if (alpha == 0.0 || k == 0) {
+    SKL_TRY(skl::launch_scale_lower<double>(C, ldc, n, beta, st));
+    return SKL_OK;
+  }
+  Bump b(workspace);
+  int k4cap = (k + 3) / 4;
+  double* P = b.take<double>(skl::packed_elems(n, k4cap));
+  double* Q = b.take<double>(skl::packed_elems(n, k4cap));
+  SKL_TRY(skl::launch_pack_rankk(A, lda, n, k, tau, alpha, nullptr, k4cap, P, Q, st));
+  SKL_TRY(skl::launch_gemm_lower(P, Q, k4cap, k4cap, nullptr, C, ldc, n, beta, st));
+  return SKL_OK;
+}
+
+int skl_form_w(int n, int k, const double* A, long long lda, const double* tau, double* W, long long ldw,
+               void* stream) {
+  if (n < 0 || k < 0 || (n > 0 && (lda < n || ldw < n))) return SKL_BAD_ARGUMENT;
+  SKL_TRY(skl::launch_form_w(A, lda, n, k, tau, W, ldw, static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+int skl_skew_rank2_lower(int n, double alpha, const double* x, const double* y, double beta, double* A,
+                         long long lda, void* stream) {
+  if (n < 0 || (n > 0 && lda < n)) return SKL_BAD_ARGUMENT;
+  if (alpha == 0.0 && beta == 1.0) return SKL_OK;
+  SKL_TRY(skl::launch_skew_rank2(A, lda, n, alpha, x, y, beta, static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+int skl_skew_tridiag_gemv(int p, int k, double alpha, const double* A, long long lda, const double* tau,
+                          const double* x, double beta, double* y, int tail_from, void* stream) {
+  if (p < 0 || k < 0 || tail_from < 0 || tail_from > p || (p > 0 && lda < p)) return SKL_BAD_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (alpha == 0.0) {
+    if (beta != 1.0) SKL_TRY(skl::launch_skew_tridiag_gemv(y, 0.0, A, lda, p, 0, tau, x, beta, tail_from, st));
+    return SKL_OK;
+  }
+  SKL_TRY(skl::launch_skew_tridiag_gemv(y, alpha, A, lda, p, k, tau, x, beta, tail_from, st));
+  return SKL_OK;
+}
+
+size_t skl_apply_row_pivots_workspace_size(int q, int lo, int hi) {
+  return (size_t)std::max(q, 1) * std::max(hi - lo, 1) * sizeof(double) + 256;
+}
+
+int skl_apply_row_pivots(int n, int q, double* block, long long ld, const long long* idx, int lo, int hi,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || q < 0 || lo < 0 || hi > n || (q > 0 && ld < n)) return SKL_BAD_ARGUMENT;
+  if (hi <= lo || q == 0) return SKL_OK;
+  if (workspace_bytes < skl_apply_row_pivots_workspace_size(q, lo, hi)) return SKL_BAD_ARGUMENT;
+  SKL_TRY(skl::launch_gather_rows(block, ld, q, lo, hi, idx, static_cast<double*>(workspace),
+                                  static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+int skl_apply_symmetric_pivot(int n, double* X, long long ld, int k, long long pi, void* stream) {
+  if (pi == 0) return SKL_OK;
+  if (pi < 0 || k < 0 || k + pi >= n) return SKL_BAD_PIVOT;
+  SKL_TRY(skl::launch_sym_swap(X, ld, n, k, (int)(k + pi), static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+// ---------------------------------------------------------------------------
+size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant) {
+  if (n < 1 || nb < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B) return 0;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, nb, variant, plan)) return 0;
+  return layout_blk(n, nb, plan, nullptr, nullptr);
+}
+
+int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
+                     double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (variant < SKL_VAR1 || variant > SKL_VAR2B) return SKL_UNSUPPORTED;
+  if (n < 1 || nb < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, nb, variant, plan)) {
+    g_last_error = "panel block does not fit the shared-memory budget";
+    return SKL_UNSUPPORTED;
+  }
+  size_t need = layout_blk(n, nb, plan, nullptr, nullptr);
+  if (workspace_bytes < need) return SKL_BAD_ARGUMENT;
+  BlkWorkspace ws;
+  layout_blk(n, nb, plan, workspace, &ws);
+  const long long ld = n;
+
+  SKL_TRY(cudaMemsetAsync(piv, 0, sizeof(long long) * n, st));
+  if (n == 1) {
+    if (L != X) SKL_TRY(cudaMemcpyAsync(L, X, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return SKL_OK;
+  }
+  SKL_TRY(cudaMemcpy2DAsync(ws.W, ld * sizeof(double), X, ldx * sizeof(double), n * sizeof(double), n,
+                            cudaMemcpyDeviceToDevice, st));
+  SKL_TRY(cudaMemsetAsync(tau, 0, sizeof(double) * (n - 1), st));
+  SKL_TRY(cudaMemsetAsync(ws.slots, 0, ws.ll_bytes, st));
+
+  // column -> last panel containing it (for the deferred row gather)
+  std::vector<int> group(n, 0);
+  for (int k = 0; k < (int)plan.size(); ++k)
+    for (int c = plan[k].lo; c < n; ++c) group[c] = k;
+  SKL_TRY(cudaMemcpyAsync(ws.col_group, group.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+
+  uint32_t tag = 1;
+  for (int k = 0; k < (int)plan.size(); ++k) {
+    const PanelPlan& p = plan[k];
+    const int rt = p.r + p.nelim;
+    const bool straggler = (variant == SKL_VAR1) && (n - rt >= 2);
+    skl::PanelArgs a{};
+    a.W = ws.W;
+    a.ld = ld;
+    a.n = n;
+    a.r = p.r;
+    a.nelim = p.nelim;
+    a.lo = p.lo;
+    a.want_y = straggler ? 1 : 0;
+    a.tau = tau;
+    a.piv = piv;
+    a.y = ws.y;
+    a.gperm = ws.gperm_all + (size_t)k * n;
+    a.disp_list = ws.disp_list;
+    a.disp_count = ws.disp_count;
+    a.side = ws.side;
+    a.slots = ws.slots;
+    a.rowa = ws.rowa;
+    a.tag0 = tag;
+    a.nblocks = p.ctas;
+    a.rows_per = p.rows_per;
+    a.kmax = p.kmax;
+    a.slot_words = ws.slot_words;
+    SKL_TRY(skl::launch_panel(a, st));
+    tag += (uint32_t)p.nelim + 1;
+
+    const int ntr = n - rt;
+    if (ntr >= 2) {
+      const int ka = rt - p.lo;
+      const int K = ka + (straggler ? 2 : 0);
+      const int nk4 = (K + 3) / 4;
+      SKL_TRY(skl::launch_pack_rankk(ws.W + (size_t)p.lo * ld + rt, ld, ntr, ka, tau + p.lo + 1, -1.0,
+                                     straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st));
+      SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, ws.W + (size_t)rt * ld + rt, ld, ntr, 1.0,
+                                     st));
+    }
+  }
+  SKL_TRY(skl::launch_compose_suffix(ws.gperm_all, (int)plan.size(), nullptr, n, ws.sigma_all, st));
+  SKL_TRY(skl::launch_finalize_l(ws.W, ld, X, ldx, L, ldl, n, ws.col_group, ws.sigma_all, L != X ? 1 : 0, st));
+  return SKL_OK;
+}
+
+// ---------------------------------------------------------------------------
+size_t skl_ltlt_unb_twostep_workspace_size(int n) { return skl::twostep_workspace_bytes(n); }
+
+int skl_ltlt_unb_twostep(int n, int pivot, const double* X, long long ldx, double* L, long long ldl, double* tau,
+                         long long* piv, int* info_dev, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
+  if (workspace_bytes < skl::twostep_workspace_bytes(n)) return SKL_BAD_ARGUMENT;
+  SKL_TRY(skl::launch_twostep(X, ldx, L, ldl, n, pivot, tau, piv, info_dev, workspace,
+                              static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+int skl_ltlt_batched_piv(int batch, int n, int dtype, const void* X, long long ldx, long long strideX, void* L,
+                         long long ldl, long long strideL, void* tau, long long* piv, double* pf_sign,
+                         double* pf_logabs, void* stream) {
+  if (batch < 0 || n < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (batch == 0) return SKL_OK;
+  if (dtype == SKL_F64) {
+    SKL_TRY(skl::launch_batched<double>(batch, n, static_cast<const double*>(X), ldx, strideX,
+                                        static_cast<double*>(L), ldl, strideL, static_cast<double*>(tau), n - 1,
+                                        piv, n, pf_sign, pf_logabs, st));
+  } else if (dtype == SKL_F32) {
+    SKL_TRY(skl::launch_batched<float>(batch, n, static_cast<const float*>(X), ldx, strideX, static_cast<float*>(L),
+                                       ldl, strideL, static_cast<float*>(tau), n - 1, piv, n, pf_sign, pf_logabs,
+                                       st));
+  } else {
+    return SKL_UNSUPPORTED;
+  }
+  return SKL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,117 @@
+// Shared device helpers for the skewltl B200 kernels (sm_100a only).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#ifndef __CUDA_ARCH__
+#define SKL_HOST_ONLY 1
+#endif
+
+namespace skl {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// LL ("low-latency") flagged words: every 8-byte word carries a 32-bit flag
+// next to 32 bits of payload, so a reader can poll the data itself and needs
+// no fence or separate flag (8-byte accesses are single-copy atomic).  A
+// double travels as two flagged words written with one 16-byte store.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ll_put2(uint64_t* p, uint32_t d0, uint32_t d1, uint32_t flag) {
+  uint64_t w0 = (uint64_t(flag) << 32) | d0;
+  uint64_t w1 = (uint64_t(flag) << 32) | d1;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+}
+
+__device__ __forceinline__ void ll_put_double(uint64_t* p, double v, uint32_t flag) {
+  uint64_t bits = __double_as_longlong(v);
+  ll_put2(p, uint32_t(bits), uint32_t(bits >> 32), flag);
+}
+
+// spin until both words carry `flag`; returns the 2 payloads
+__device__ __forceinline__ void ll_get2(const uint64_t* p, uint32_t flag, uint32_t& d0, uint32_t& d1) {
+  uint64_t w0, w1;
+  do {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+  } while (uint32_t(w0 >> 32) != flag || uint32_t(w1 >> 32) != flag);
+  d0 = uint32_t(w0);
+  d1 = uint32_t(w1);
+}
+
+__device__ __forceinline__ double ll_get_double(const uint64_t* p, uint32_t flag) {
+  uint32_t lo, hi;
+  ll_get2(p, flag, lo, hi);
+  return __longlong_as_double((long long)((uint64_t(hi) << 32) | lo));
+}
+
+// ---------------------------------------------------------------------------
+// FP64 tensor pipe: DMMA.8x8x4.  Fragment layout (lane l):
+//   A (8x4, row): a = A[l/4][l%4];  B (4x8, col): b = B[l%4][l/4]
+//   C/D (8x8): d0 = D[l/4][2(l%4)], d1 = D[l/4][2(l%4)+1]
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk async copy (TMA bulk engine, UBLKCP)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// global -> shared bulk copy, completion signalled on `bar` (bytes multiple of 16)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// skew-lower element access: X(p, q) of the full skew matrix whose strictly
+// lower triangle is stored column-major in W (p != q).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T skew_at(const T* __restrict__ W, long long ld, int p, int q) {
+  return p > q ? W[(long long)q * ld + p] : -W[(long long)p * ld + q];
+}
+
+}  // namespace skl

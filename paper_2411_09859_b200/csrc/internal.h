@@ -1,0 +1,95 @@
+// Internal (non-exported) launchers shared between the translation units of
+// libskewltl_b200.so.  Every launcher enqueues on `stream` and never syncs.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace skl {
+
+// ---- packed operand layout for the lower-triangular DGEMM-NT --------------
+// An operand X (rows x K) is stored as 128-row tiles; inside a tile, K is
+// split into k4 blocks of 4 columns and rows into 16 blocks of 8; the 32
+// doubles of an (8 x 4) block are in DMMA-fragment lane order
+// (lane = 4*(row%8) + col%4).  One k4 block of one tile is 4 KiB contiguous.
+constexpr int kTile = 128;
+__host__ __device__ inline int tiles_for(int rows) { return (rows + kTile - 1) / kTile; }
+__host__ __device__ inline size_t packed_elems(int rows, int k4cap) { return (size_t)tiles_for(rows) * kTile * 4 * k4cap; }
+
+// C[i,j] (i>j, i,j < n) = beta*C[i,j] + sum_k P[i,k] Q[j,k]
+// nk4_dev (optional) overrides nk4 with a device-resident count.
+cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
+                              double* C, long long ldc, int n, double beta, cudaStream_t stream);
+
+// P = alpha*A, Q = A T^T with T tridiag(t) (t = tau_base[0..ka-2]); optional
+// var1 straggler columns (l = A[:, ka-1], y) zeroed on row 0.
+cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, const double* tau_base,
+                              double alpha, const double* y, int k4cap, double* P, double* Q,
+                              cudaStream_t stream);
+
+// skr2k: keep[] (device) lists columns nonzero in both A and B; count at keff_dev.
+cudaError_t launch_rank2k_keep(const double* A, long long lda, const double* B, long long ldb, int n, int k,
+                               int skip_zero, int* keep, int* keff_dev, int* nk4_dev, cudaStream_t stream);
+cudaError_t launch_pack_rank2k(const double* A, long long lda, const double* B, long long ldb, int n, int k,
+                               double alpha, const int* keep, const int* keff_dev, int k4cap, double* P,
+                               double* Q, cudaStream_t stream);
+
+cudaError_t launch_form_w(const double* A, long long lda, int n, int k, const double* tau, double* W,
+                          long long ldw, cudaStream_t stream);
+
+// ---- level-2 kernels ------------------------------------------------------
+cudaError_t launch_skew_rank2(double* A, long long lda, int n, double alpha, const double* x, const double* y,
+                              double beta, cudaStream_t stream);
+cudaError_t launch_skew_tridiag_gemv(double* y, double alpha, const double* A, long long lda, int p, int k,
+                                     const double* tau, const double* x, double beta, int tail_from,
+                                     cudaStream_t stream);
+cudaError_t launch_gather_rows(double* block, long long ld, int q, int lo, int hi, const long long* idx_dev,
+                               double* tmp, cudaStream_t stream);
+cudaError_t launch_sym_swap(double* X, long long ld, int n, int a, int b, cudaStream_t stream);
+template <typename T>
+cudaError_t launch_scale_lower(T* C, long long ldc, int n, T beta, cudaStream_t stream);
+
+// ---- factorization pieces -------------------------------------------------
+struct PanelArgs {
+  double* W;             // n x n work buffer (lower storage, column-major)
+  long long ld;
+  int n;
+  int r, nelim, lo;      // eliminate columns [r, r+nelim); leftmost participating column lo
+  int want_y;            // var1: compute y = column rt after the trailing couplings
+  double* tau;           // device tau (length n-1)
+  long long* piv;        // device pivots (length n)
+  double* y;             // device y vector (position indexed), var1 only
+  int* gperm;            // out: position -> physical map of this panel (length n)
+  int* disp_list;        // scratch: displaced trailing positions
+  int* disp_count;       // scratch counter (zeroed by the kernel launcher)
+  double* side;          // scratch: displaced trailing lines (2*nelim x n)
+  uint64_t* slots;       // LL exchange area
+  uint64_t* rowa;        // LL exchange area for the row being displaced
+  uint32_t tag0;         // first LL tag of this panel
+  int nblocks;           // CTAs (co-resident)
+  int rows_per;          // rows per CTA
+  int kmax;              // slab columns (= r + nelim - lo)
+  int slot_words;
+};
+size_t panel_smem_bytes(int rows_per, int kmax);
+int panel_max_ctas();
+int panel_threads();
+cudaError_t launch_panel(const PanelArgs& a, cudaStream_t stream);
+
+cudaError_t launch_compose_suffix(const int* gperm_all, int npanels, const int* row0s, int n, int* sigma_all,
+                                  cudaStream_t stream);
+cudaError_t launch_finalize_l(const double* W, long long ldw, const double* X, long long ldx, double* L,
+                              long long ldl, int n, const int* col_group, const int* sigma_all, int copy_upper,
+                              cudaStream_t stream);
+
+// ---- unblocked two-step (config 1) and batched (config 4) ------------------
+cudaError_t launch_twostep(const double* X, long long ldx, double* L, long long ldl, int n, int pivot,
+                           double* tau, long long* piv, int* info, void* workspace, cudaStream_t stream);
+size_t twostep_workspace_bytes(int n);
+
+template <typename T>
+cudaError_t launch_batched(int batch, int n, const T* X, long long ldx, long long strideX, T* L, long long ldl,
+                           long long strideL, T* tau, long long strideTau, long long* piv, long long stridePiv,
+                           double* pf_sign, double* pf_logabs, cudaStream_t stream);
+
+}  // namespace skl

@@ -1,0 +1,317 @@
+// Trailing "sandwiched" update on the FP64 tensor pipe.
+//
+// The reference realizes C := C - A T A^T (kernels3.py:151-209,
+// skew_tridiag_rankk) and C := C + alpha (A B^T - B A^T) (kernels3.py:305-351,
+// skew_rank2k) as Goto-blocked NumPy/OpenBLAS tiles with a masked merge on
+// diagonal tiles.  Here both are ONE lower-triangular DGEMM-NT
+//     C[i,j] = beta*C[i,j] + sum_k P[i,k] Q[j,k]      (i > j only)
+// whose operands P, Q are packed by a small kernel that also forms the
+// tridiagonal-multiplied operand (B = A T^T, or W = A S for skr2k) on the fly,
+// the GPU analogue of the reference's "T rides along with packing"
+// (_pack_bt_panel, kernels3.py:134-148).
+//
+// GEMM kernel: 128x128 C tile per CTA, 8 compute warps in a 2x4 grid of
+// 64x32 warp tiles, DMMA.8x8x4 (mma.sync m8n8k4 f64).  Operand k-chunks are
+// streamed by the bulk-copy engine (cp.async.bulk -> mbarrier complete_tx)
+// through a 4-stage shared-memory ring; the packed layout puts every DMMA
+// fragment in lane order so fragment loads are conflict-free 256-byte rows.
+// Only lower tiles are launched (triangle-aware schedule); diagonal tiles
+// mask i <= j at load and store, so the upper triangle is never read or
+// written (test_core.py:39-58 NaN-poison invariant).
+#include "common.cuh"
+#include "internal.h"
+
+namespace skl {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kK4PerStage = 4;                    // 16 k per stage
+constexpr int kBlkDoubles = 16 * 32;              // one k4 block of a 128-row tile
+constexpr int kStageDoubles = kK4PerStage * kBlkDoubles;
+constexpr int kGemmThreads = 256;
+constexpr size_t kGemmSmem = size_t(kStages) * 2 * kStageDoubles * sizeof(double) + 64;
+
+__device__ __forceinline__ size_t packed_off(int row, int col, int k4cap) {
+  int t = row >> 7, mb = (row >> 3) & 15, r8 = row & 7;
+  int q = col >> 2, c4 = col & 3;
+  return (((size_t)t * k4cap + q) * 16 + mb) * 32 + (r8 * 4 + c4);
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q, int k4cap, int nk4_host,
+                     const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sP = reinterpret_cast<double*>(smem_raw);
+  double* sQ = sP + kStages * kStageDoubles;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + kStages * kStageDoubles);
+
+  // triangular tile index -> (ti, tj), ti >= tj
+  const int t = blockIdx.x;
+  int ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  const int tj = t - ti * (ti + 1) / 2;
+
+  const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
+  const int nchunks = (nk4 + kK4PerStage - 1) / kK4PerStage;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 2, wn = warp & 3;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const double* Pt = P + (size_t)ti * k4cap * kBlkDoubles;
+  const double* Qt = Q + (size_t)tj * k4cap * kBlkDoubles;
+  auto issue = [&](int chunk) {
+    int s = chunk % kStages;
+    int q0 = chunk * kK4PerStage;
+    int nb = min(kK4PerStage, nk4 - q0);
+    uint32_t bytes = uint32_t(nb) * kBlkDoubles * sizeof(double);
+    mbar_arrive_expect_tx(&full[s], 2 * bytes);
+    bulk_g2s(sP + s * kStageDoubles, Pt + (size_t)q0 * kBlkDoubles, bytes, &full[s]);
+    bulk_g2s(sQ + s * kStageDoubles, Qt + (size_t)q0 * kBlkDoubles, bytes, &full[s]);
+  };
+  if (tid == 0) {
+    for (int c = 0; c < min(kStages, nchunks); ++c) issue(c);
+  }
+
+  // accumulators initialised from beta*C (masked to the strictly-lower part)
+  double acc[8][4][2];
+  const int row_base = ti * kTile + wm * 64 + (lane >> 2);
+  const int col_base = tj * kTile + wn * 32 + 2 * (lane & 3);
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int row = row_base + mi * 8, col = col_base + ni * 8 + e;
+        double v = 0.0;
+        if (beta != 0.0 && row < n && col < n && row > col) v = beta * C[(long long)col * ldc + row];
+        acc[mi][ni][e] = v;
+      }
+    }
+  }
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int s = c % kStages;
+    mbar_wait(&full[s], (c / kStages) & 1);
+    const int nb = min(kK4PerStage, nk4 - c * kK4PerStage);
+    const double* ps = sP + s * kStageDoubles + (wm * 8) * 32 + lane;
+    const double* qs = sQ + s * kStageDoubles + (wn * 4) * 32 + lane;
+    for (int kb = 0; kb < nb; ++kb) {
+      double a[8], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) a[mi] = ps[kb * kBlkDoubles + mi * 32];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = qs[kb * kBlkDoubles + ni * 32];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (tid == 0 && c + kStages < nchunks) {
+      fence_proxy_async();
+      issue(c + kStages);
+    }
+  }
+
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int row = row_base + mi * 8, col = col_base + ni * 8 + e;
+        if (row < n && col < n && row > col) C[(long long)col * ldc + row] = acc[mi][ni][e];
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void packed_decode(size_t off, int k4cap, int& row, int& col) {
+  int lane = int(off & 31);
+  int mb = int((off >> 5) & 15);
+  size_t rest = off >> 9;
+  int q = int(rest % (size_t)k4cap);
+  int t = int(rest / (size_t)k4cap);
+  row = t * kTile + mb * 8 + (lane >> 2);
+  col = q * 4 + (lane & 3);
+}
+
+// P = alpha*A, Q[:, j] = t[j-1] A[:, j-1] - t[j] A[:, j+1]   (Q = A T^T, T = tridiag(t))
+// optional var1 straggler pair (rows >= 1 only; l = A[:, ka-1]):
+//   P[:, ka] = l,  P[:, ka+1] = -y,  Q[:, ka] = y,  Q[:, ka+1] = l
+// so that sum_k P Q^T = alpha A T A^T + l y^T - y l^T.
+__global__ void pack_rankk_kernel(const double* __restrict__ A, long long lda, int rows, int ka,
+                                  const double* __restrict__ t, double alpha, const double* __restrict__ y,
+                                  int k4cap, double* __restrict__ P, double* __restrict__ Q) {
+  const size_t total = (size_t)tiles_for(rows) * kTile * 4 * k4cap;
+  for (size_t off = blockIdx.x * (size_t)blockDim.x + threadIdx.x; off < total;
+       off += (size_t)gridDim.x * blockDim.x) {
+    int row, col;
+    packed_decode(off, k4cap, row, col);
+    double p = 0.0, q = 0.0;
+    if (row < rows) {
+      if (col < ka) {
+        const double* ar = A + row;
+        p = alpha * ar[(long long)col * lda];
+        double acc = 0.0;
+        if (col >= 1) acc = t[col - 1] * ar[(long long)(col - 1) * lda];
+        if (col + 1 < ka) acc -= t[col] * ar[(long long)(col + 1) * lda];
+        q = acc;
+      } else if (y != nullptr && row >= 1 && col < ka + 2) {
+        double lv = A[(long long)(ka - 1) * lda + row];
+        double yv = y[row];
+        if (col == ka) {
+          p = lv;
+          q = yv;
+        } else {
+          p = -yv;
+          q = lv;
+        }
+      }
+    }
+    P[off] = p;
+    Q[off] = q;
+  }
+}
+
+// keep[j] = column j is nonzero in both A and B (kernels3.py:318-321);
+// single CTA: flags, then an ordered compaction.
+__global__ void rank2k_keep_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B,
+                                   long long ldb, int n, int k, int skip_zero, int* __restrict__ keep,
+                                   int* __restrict__ keff_dev, int* __restrict__ nk4_dev) {
+  extern __shared__ int flags[];
+  for (int j = threadIdx.x >> 5; j < k; j += blockDim.x >> 5) {
+    int lane = threadIdx.x & 31;
+    int nzA = 0, nzB = 0;
+    if (skip_zero) {
+      for (int i = lane; i < n; i += 32) {
+        nzA |= A[(long long)j * lda + i] != 0.0;
+        nzB |= B[(long long)j * ldb + i] != 0.0;
+      }
+      nzA = __any_sync(0xffffffffu, nzA);
+      nzB = __any_sync(0xffffffffu, nzB);
+    } else {
+      nzA = nzB = 1;
+    }
+    if (lane == 0) flags[j] = nzA && nzB;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int j = 0; j < k; ++j)
+      if (flags[j]) keep[c++] = j;
+    *keff_dev = c;
+    *nk4_dev = (2 * c + 3) / 4;
+  }
+}
+
+// P = alpha*[A_keep | B_keep], Q = [B_keep | -A_keep]  => sum P Q^T = alpha (A B^T - B A^T)
+__global__ void pack_rank2k_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B,
+                                   long long ldb, int n, double alpha, const int* __restrict__ keep,
+                                   const int* __restrict__ keff_dev, int k4cap, double* __restrict__ P,
+                                   double* __restrict__ Q) {
+  const int keff = *keff_dev;
+  const size_t total = (size_t)tiles_for(n) * kTile * 4 * k4cap;
+  for (size_t off = blockIdx.x * (size_t)blockDim.x + threadIdx.x; off < total;
+       off += (size_t)gridDim.x * blockDim.x) {
+    int row, col;
+    packed_decode(off, k4cap, row, col);
+    double p = 0.0, q = 0.0;
+    if (row < n && col < 2 * keff) {
+      int j = keep[col < keff ? col : col - keff];
+      double av = A[(long long)j * lda + row], bv = B[(long long)j * ldb + row];
+      if (col < keff) {
+        p = alpha * av;
+        q = bv;
+      } else {
+        p = alpha * bv;
+        q = -av;
+      }
+    }
+    P[off] = p;
+    Q[off] = q;
+  }
+}
+
+// W = A S with T = S - S^T (core.py:153-169, kernels3.py:354-364):
+// even columns zero; odd j: W[:, j] = -tau[j-1] A[:, j-1] + tau[j] A[:, j+1] (second term if j+1 < k)
+__global__ void form_w_kernel(const double* __restrict__ A, long long lda, int n, int k,
+                              const double* __restrict__ tau, double* __restrict__ W, long long ldw) {
+  const size_t total = (size_t)n * k;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    int j = int(e / n), i = int(e % n);
+    double w = 0.0;
+    if (j & 1) {
+      w = -tau[j - 1] * A[(long long)(j - 1) * lda + i];
+      if (j + 1 < k) w += tau[j] * A[(long long)(j + 1) * lda + i];
+    }
+    W[(long long)j * ldw + i] = w;
+  }
+}
+
+int grid_for(size_t total, int threads) {
+  size_t g = (total + threads - 1) / threads;
+  if (g > 148 * 16) g = 148 * 16;
+  return int(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
+                              double* C, long long ldc, int n, double beta, cudaStream_t stream) {
+  if (n < 2) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_lower_nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kGemmSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  int nt = tiles_for(n);
+  int ntiles = nt * (nt + 1) / 2;
+  gemm_lower_nt_kernel<<<ntiles, kGemmThreads, kGemmSmem, stream>>>(P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, const double* tau_base,
+                              double alpha, const double* y, int k4cap, double* P, double* Q,
+                              cudaStream_t stream) {
+  size_t total = packed_elems(rows, k4cap);
+  pack_rankk_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, rows, ka, tau_base, alpha, y, k4cap, P, Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rank2k_keep(const double* A, long long lda, const double* B, long long ldb, int n, int k,
+                               int skip_zero, int* keep, int* keff_dev, int* nk4_dev, cudaStream_t stream) {
+  rank2k_keep_kernel<<<1, 1024, sizeof(int) * (k > 0 ? k : 1), stream>>>(A, lda, B, ldb, n, k, skip_zero, keep,
+                                                                        keff_dev, nk4_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_rank2k(const double* A, long long lda, const double* B, long long ldb, int n, int k,
+                               double alpha, const int* keep, const int* keff_dev, int k4cap, double* P,
+                               double* Q, cudaStream_t stream) {
+  (void)k;
+  size_t total = packed_elems(n, k4cap);
+  pack_rank2k_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, B, ldb, n, alpha, keep, keff_dev, k4cap, P,
+                                                               Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_form_w(const double* A, long long lda, int n, int k, const double* tau, double* W,
+                          long long ldw, cudaStream_t stream) {
+  size_t total = (size_t)n * k;
+  if (total == 0) return cudaSuccess;
+  form_w_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, n, k, tau, W, ldw);
+  return cudaGetLastError();
+}
+
+}  // namespace skl
