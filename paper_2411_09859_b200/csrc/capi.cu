@@ -7,6 +7,7 @@
 // panel, one gather applies the deferred row interchanges to the L columns.
 // Everything is enqueued on the caller's stream with no host synchronisation.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -18,6 +19,7 @@
 namespace {
 
 thread_local std::string g_last_error;
+unsigned long long* g_prof = nullptr;  // debug: panel phase profile (device)
 
 int fail_cuda(cudaError_t e, const char* where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -62,6 +64,7 @@ size_t mat_bytes(int rows, int cols, long long ld) {
 struct PanelPlan {
   int r, nelim, lo;
   int ctas, rows_per, kmax;
+  int cluster;  // 1: single-cluster DSMEM panel kernel, 0: grid-wide kernel
 };
 
 size_t smem_limit() {
@@ -75,9 +78,28 @@ size_t smem_limit() {
   return (size_t)lim;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int rows = n - (lo + 1);
-  int ctas = (rows + 7) / 8;
+  static int no_cluster = env_int("SKL_NO_CLUSTER", 0);
+  const int C = no_cluster ? 0 : skl::panel_cluster_size();
+  if (C > 0) {
+    int Rc = (rows + C - 1) / C;
+    if (Rc <= 1024) {
+      int w = want;
+      while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo) > smem_limit()) --w;
+      if (w >= 1 && w >= std::min(want, 64)) {
+        p = PanelPlan{r, w, lo, C, Rc, r + w - lo, 1};
+        return true;
+      }
+    }
+  }
+  static int min_rows = env_int("SKL_PANEL_MIN_ROWS", 8);
+  int ctas = (rows + min_rows - 1) / min_rows;
   if (ctas > nsm) ctas = nsm;
   if (ctas < 1) ctas = 1;
   int R = (rows + ctas - 1) / ctas;
@@ -85,7 +107,7 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int nelim = want;
   while (nelim >= 1 && skl::panel_smem_bytes(R, r + nelim - lo) > smem_limit()) --nelim;
   if (nelim < 1) return false;
-  p = PanelPlan{r, nelim, lo, ctas, R, r + nelim - lo};
+  p = PanelPlan{r, nelim, lo, ctas, R, r + nelim - lo, 0};
   return true;
 }
 
@@ -132,6 +154,9 @@ struct BlkWorkspace {
   int* disp_count;
   uint64_t* slots;
   uint64_t* rowa;
+  uint64_t* recs;
+  double* crow;
+  double* arowg;
   size_t ll_bytes;
   int k4cap, slot_words, np;
 };
@@ -162,6 +187,9 @@ size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base,
   size_t ll_start = align_up(b.off);
   w.slots = b.take<uint64_t>((size_t)ctas * 2 * slot_words);
   w.rowa = b.take<uint64_t>((size_t)2 * slot_words);
+  w.recs = b.take<uint64_t>((size_t)2 * ctas * 4);
+  w.crow = b.take<double>((size_t)2 * 16 * (kmax + 2));
+  w.arowg = b.take<double>((size_t)2 * (kmax + 2));
   w.ll_bytes = b.off - ll_start;
   w.k4cap = k4cap;
   w.slot_words = slot_words;
@@ -176,6 +204,12 @@ extern "C" {
 
 const char* skl_version(void) { return "skewltl_b200 0.1.0 (sm_100a)"; }
 const char* skl_last_error(void) { return g_last_error.c_str(); }
+
+// debug hook: route per-CTA panel phase cycle counters to a device buffer (NULL disables)
+int skl_debug_set_panel_profile(unsigned long long* dev_buf) {
+  g_prof = dev_buf;
+  return SKL_OK;
+}
 
 // ---------------------------------------------------------------------------
 size_t skl_skr2k_workspace_size(int n, int k) {
@@ -365,12 +399,21 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     a.side = ws.side;
     a.slots = ws.slots;
     a.rowa = ws.rowa;
+    a.recs = ws.recs;
+    a.crow = ws.crow;
+    a.arowg = ws.arowg;
     a.tag0 = tag;
     a.nblocks = p.ctas;
     a.rows_per = p.rows_per;
     a.kmax = p.kmax;
     a.slot_words = ws.slot_words;
-    SKL_TRY(skl::launch_panel(a, st));
+    static int dbg = env_int("SKL_PANEL_DBG", 0);
+    a.dbg = dbg;
+    a.prof = g_prof;
+    if (p.cluster)
+      SKL_TRY(skl::launch_panel_cluster(a, st));
+    else
+      SKL_TRY(skl::launch_panel(a, st));
     tag += (uint32_t)p.nelim + 1;
 
     const int ntr = n - rt;

@@ -20,7 +20,7 @@ constexpr int kWarp = 32;
 __device__ __forceinline__ void ll_put2(uint64_t* p, uint32_t d0, uint32_t d1, uint32_t flag) {
   uint64_t w0 = (uint64_t(flag) << 32) | d0;
   uint64_t w1 = (uint64_t(flag) << 32) | d1;
-  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(w0), "l"(w1) : "memory");
 }
 
 __device__ __forceinline__ void ll_put_double(uint64_t* p, double v, uint32_t flag) {
@@ -32,7 +32,7 @@ __device__ __forceinline__ void ll_put_double(uint64_t* p, double v, uint32_t fl
 __device__ __forceinline__ void ll_get2(const uint64_t* p, uint32_t flag, uint32_t& d0, uint32_t& d1) {
   uint64_t w0, w1;
   do {
-    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
   } while (uint32_t(w0 >> 32) != flag || uint32_t(w1 >> 32) != flag);
   d0 = uint32_t(w0);
   d1 = uint32_t(w1);

@@ -65,16 +65,25 @@ struct PanelArgs {
   double* side;          // scratch: displaced trailing lines (2*nelim x n)
   uint64_t* slots;       // LL exchange area
   uint64_t* rowa;        // LL exchange area for the row being displaced
+  uint64_t* recs;        // LL candidate records [2][P][4]
+  double* crow;          // cluster panel: candidate rows [2][C][kmax+2]
+  double* arowg;         // cluster panel: row a [2][kmax+2]
   uint32_t tag0;         // first LL tag of this panel
   int nblocks;           // CTAs (co-resident)
   int rows_per;          // rows per CTA
   int kmax;              // slab columns (= r + nelim - lo)
   int slot_words;
+  int dbg;               // timing experiments only (bitmask of skipped phases)
+  unsigned long long* prof;  // optional per-CTA phase cycle totals [C][8]
 };
 size_t panel_smem_bytes(int rows_per, int kmax);
 int panel_max_ctas();
 int panel_threads();
 cudaError_t launch_panel(const PanelArgs& a, cudaStream_t stream);
+// single-cluster variant (DSMEM exchange); cluster size 16 (or 8), 0 if unavailable
+int panel_cluster_size();
+size_t panel_cluster_smem_bytes(int rows_per, int kmax);
+cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
 
 cudaError_t launch_compose_suffix(const int* gperm_all, int npanels, const int* row0s, int n, int* sigma_all,
                                   cudaStream_t stream);

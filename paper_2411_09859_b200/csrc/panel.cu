@@ -39,6 +39,35 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxZ = 16;  // z register slots per lane -> kmax <= 512
 
+#ifdef SKL_PANEL_PROFILE
+__device__ unsigned long long g_panel_prof[2][16];
+__device__ unsigned long long g_panel_ts[8][160][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TS_MARK(slot)                                                               \
+  do {                                                                              \
+    if (tid == 0 && r == 0 && g >= 100 && g < 108 && cta < 160) g_panel_ts[g - 100][cta][slot] = gtime(); \
+  } while (0)
+#define PROF_MARK(ph)                                                        \
+  do {                                                                       \
+    if (tid == 0 && (cta == 0 || cta == P - 1)) {                            \
+      long long _t = clock64();                                              \
+      atomicAdd(&g_panel_prof[cta == 0 ? 0 : 1][ph], (unsigned long long)(_t - _pt)); \
+      _pt = _t;                                                              \
+    }                                                                        \
+  } while (0)
+#else
+#define TS_MARK(slot) \
+  do {                \
+  } while (0)
+#define PROF_MARK(ph) \
+  do {                \
+  } while (0)
+#endif
+
 struct __align__(16) Cand {
   double v;
   int idx;
@@ -72,16 +101,18 @@ struct Smem {
   double* wrow;   // winner row / pivot row x   [kmax + 2]
   double* arow;   // row a (displaced row)      [kmax + 2]
   double* taus;   // taus[j] = tau[lo + j]      [kmax + 2]
+  double* zbuf;   // z = T x for the next gemv  [kmax + 2]
+  double* part;   // gemv partial sums          [kThreads]
   double* ycol;   // scratch column             [Rs]
   int* perm;      // position -> physical       [Rs]
   Cand* wcand;    // per-warp candidates        [kWarps]
-  Cand* ccand;    // per-CTA candidates         [P]
-  int* misc;      // [0]=winner cta, [1]=winner idx, [2]=winner perm, [3]=perm_a
+  int* misc;      // [0]=winner cta, [1]=winner idx, [2]=winner perm, [3]=perm_a, [4..7] cta cand
 };
 
 __host__ __device__ inline int slab_stride(int rows_per) { return rows_per | 1; }
 
 __host__ __device__ inline size_t smem_layout(int rows_per, int kmax, int P, Smem* s, unsigned char* base) {
+  (void)P;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -98,57 +129,61 @@ __host__ __device__ inline size_t smem_layout(int rows_per, int kmax, int P, Sme
   if (s) s->arow = (double*)p;
   p = take(sizeof(double) * (kmax + 2));
   if (s) s->taus = (double*)p;
+  p = take(sizeof(double) * (kmax + 2));
+  if (s) s->zbuf = (double*)p;
+  p = take(sizeof(double) * kThreads);
+  if (s) s->part = (double*)p;
   p = take(sizeof(double) * Rs);
   if (s) s->ycol = (double*)p;
   p = take(sizeof(int) * Rs);
   if (s) s->perm = (int*)p;
   p = take(sizeof(Cand) * kWarps);
   if (s) s->wcand = (Cand*)p;
-  p = take(sizeof(Cand) * P);
-  if (s) s->ccand = (Cand*)p;
   p = take(sizeof(int) * 8);
   if (s) s->misc = (int*)p;
   return off;
 }
 
-// v[li] = c[li] - sum_j slab[j][li] z_j  for local rows li in [l0, R), written
-// in place into slab column k (which holds c on entry).  z = T x with
-// T = tridiag(taus[1..k-1]), x = wrow[0..k-1].  Returns per-lane best
-// candidate over processed rows (lane 0 only meaningful after warp reduce).
-__device__ __forceinline__ void gemv_rows(const Smem& s, int Rs, int k, int l0, int R, int rbase, int warp,
-                                          int lane, double* outcol, Cand& best) {
-  double z[kMaxZ];
-#pragma unroll
-  for (int m = 0; m < kMaxZ; ++m) {
-    int j = lane + 32 * m;
-    double zz = 0.0;
-    if (j < k) {
-      if (j >= 1) zz = s.taus[j] * s.wrow[j - 1];
-      if (j + 1 < k) zz -= s.taus[j + 1] * s.wrow[j + 1];
+// Partial left-looking products: part[gi*R + li] = sum_{j in group gi} slab[j][li] z_j.
+// G groups of R threads split the k columns (short FMA chains, 2 accumulators).
+__device__ __forceinline__ void gemv_partials(const Smem& s, int Rs, int R, int G, int k, int l0, int tid) {
+  if (G > 1) {
+    if (tid < G * R) {
+      const int gi = tid / R, li = tid - gi * R;
+      if (li >= l0) {
+        const int kc = (k + G - 1) / G;
+        const int j0 = gi * kc, j1 = min(k, j0 + kc);
+        double a0 = 0.0, a1 = 0.0;
+        int j = j0;
+        for (; j + 1 < j1; j += 2) {
+          a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
+          a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
+        }
+        if (j < j1) a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
+        s.part[gi * R + li] = a0 + a1;
+      }
     }
-    z[m] = zz;
   }
-  const int nm = (k + 31) >> 5;
-  for (int li = l0 + warp; li < R; li += kWarps) {
+}
+
+// v = c - sum of partials (or the full dot product when G == 1), for local row li
+__device__ __forceinline__ double gemv_finish(const Smem& s, int Rs, int R, int G, int k, int li, double c) {
+  if (k < 2) return c;
+  if (G > 1) {
     double acc = 0.0;
-#pragma unroll
-    for (int m = 0; m < kMaxZ; ++m) {
-      if (m < nm) {
-        int j = lane + 32 * m;
-        if (j < k) acc = fma(s.slab[(size_t)j * Rs + li], z[m], acc);
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      double v = outcol[li] - acc;
-      outcol[li] = v;
-      if (better(v, rbase + li, best.v, best.idx)) {
-        best.v = v;
-        best.idx = rbase + li;
-      }
-    }
+    for (int gi = 0; gi < G; ++gi) acc += s.part[gi * R + li];
+    return c - acc;
   }
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int j = 0;
+  for (; j + 3 < k; j += 4) {
+    a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
+    a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
+    a2 = fma(s.slab[(size_t)(j + 2) * Rs + li], s.zbuf[j + 2], a2);
+    a3 = fma(s.slab[(size_t)(j + 3) * Rs + li], s.zbuf[j + 3], a3);
+  }
+  for (; j < k; ++j) a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
+  return c - ((a0 + a1) + (a2 + a3));
 }
 
 __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
@@ -158,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n, lo = a.lo, r = a.r, nelim = a.nelim, kmax = a.kmax;
   const int R = a.rows_per, Rs = slab_stride(R);
+  const int G = R <= kThreads ? max(1, min(kThreads / max(R, 1), 16)) : 1;
   const long long ld = a.ld;
   double* __restrict__ W = a.W;
   const int row0 = lo + 1;
@@ -176,8 +212,8 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
   for (int j = tid; j < kmax + 2; j += kThreads) {
     s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
     s.wrow[j] = 0.0;
+    s.zbuf[j] = 0.0;
   }
-  // first column g = r: X_cur[i, r] = X0[i, r] for i > r
   {
     double* col = s.slab + (size_t)(r - lo) * Rs;
     for (int li = tid; li < rcount; li += kThreads) {
@@ -185,126 +221,158 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
       col[li] = pos > r ? W[(long long)r * ld + pos] : 0.0;
     }
   }
-  int pg = r;  // physical index of the current column's position
   __syncthreads();
 
   const int slot_words = a.slot_words;
+  long long _pt = clock64();
+  (void)_pt;
   for (int g = r; g < rt; ++g) {
     const int k = g - lo;  // slab column of the current column
     const uint32_t tag = a.tag0 + uint32_t(g - r);
     const int par = tag & 1;
     double* col = s.slab + (size_t)k * Rs;
     const int l_first = max(0, g + 1 - rbase);  // first local row with position >= g+1
+    const int a_pos = g + 1;
+    const bool own_a = a_pos >= rbase && a_pos < rbase + rcount;
+    TS_MARK(0);
 
-    // ---- left-looking update + local argmax ------------------------------
+    // ---- A/B: left-looking update v = c - A z, local argmax -----------------
+    const int kk = (a.dbg & 1) ? 0 : k;
+    if (kk >= 2 && G > 1) {
+      gemv_partials(s, Rs, R, G, kk, l_first, tid);
+      __syncthreads();
+    }
     Cand best;
     best.v = 0.0;
     best.idx = -1;
     best.perm = -1;
-    if (k >= 2) {
-      gemv_rows(s, Rs, k, l_first, rcount, rbase, warp, lane, col, best);
-    } else {
-      for (int li = l_first + tid; li < rcount; li += kThreads) {
-        double v = col[li];
-        if (better(v, rbase + li, best.v, best.idx)) {
-          best.v = v;
-          best.idx = rbase + li;
-        }
+    for (int li = l_first + tid; li < rcount; li += kThreads) {
+      double v = gemv_finish(s, Rs, R, G, kk, li, col[li]);
+      col[li] = v;
+      if (better(v, rbase + li, best.v, best.idx)) {
+        best.v = v;
+        best.idx = rbase + li;
+        best.perm = s.perm[li];
       }
     }
+    PROF_MARK(0);
     warp_argmax(best.v, best.idx, best.perm);
     if (lane == 0) s.wcand[warp] = best;
     __syncthreads();
+    PROF_MARK(1);
+
+    // ---- C: publish (warp 0: candidate + row; warp 1: row a), poll, reduce ----
     if (warp == 0) {
       Cand c = lane < kWarps ? s.wcand[lane] : Cand{0.0, -1, -1};
       warp_argmax(c.v, c.idx, c.perm);
-      if (lane == 0) {
-        if (c.idx >= 0) c.perm = s.perm[c.idx - rbase];
-        s.misc[4] = c.idx;
-        s.misc[5] = c.perm;
-        reinterpret_cast<double*>(s.misc + 6)[0] = c.v;  // misc[6..7]
-      }
-    }
-    __syncthreads();
-
-    // ---- publish candidate (+ its row) and, if owned, row a ---------------
-    const int a_pos = g + 1;
-    const bool own_a = a_pos >= rbase && a_pos < rbase + rcount;
-    {
       uint64_t* slot = a.slots + ((size_t)cta * 2 + par) * slot_words;
-      const int cidx = s.misc[4];
-      if (cidx >= 0) {
-        const int lc = cidx - rbase;
-        for (int j = tid; j <= k; j += kThreads) ll_put_double(slot + 4 + 2 * j, s.slab[(size_t)j * Rs + lc], tag);
+      uint64_t* rec = a.recs + ((size_t)par * P + cta) * 4;
+      if (c.idx >= 0 && !(a.dbg & 8)) {
+        const int lc = c.idx - rbase;
+        for (int j = lane; j <= k; j += 32) ll_put_double(slot + 4 + 2 * j, s.slab[(size_t)j * Rs + lc], tag);
       }
-      if (own_a) {
-        uint64_t* ra = a.rowa + (size_t)par * slot_words;
-        const int la = a_pos - rbase;
-        for (int j = tid; j <= k; j += kThreads) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
-        if (tid == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
+      if (lane == 0) {
+        uint64_t bits = __double_as_longlong(c.v);
+        ll_put2(rec + 2, uint32_t(c.idx), uint32_t(c.perm), tag);
+        ll_put2(rec, uint32_t(bits), uint32_t(bits >> 32), tag);
       }
-      if (tid == 0) {
-        double cv = reinterpret_cast<double*>(s.misc + 6)[0];
-        uint64_t bits = __double_as_longlong(cv);
-        ll_put2(slot, uint32_t(bits), uint32_t(bits >> 32), tag);
-        ll_put2(slot + 2, uint32_t(cidx), uint32_t(s.misc[5]), tag);
-      }
-    }
-
-    // ---- poll every CTA's candidate ---------------------------------------
-    for (int t = tid; t < P; t += kThreads) {
-      const uint64_t* slot = a.slots + ((size_t)t * 2 + par) * slot_words;
-      uint32_t lo32, hi32, ci, cp;
-      ll_get2(slot, tag, lo32, hi32);
-      ll_get2(slot + 2, tag, ci, cp);
-      Cand c;
-      c.v = __longlong_as_double((long long)((uint64_t(hi32) << 32) | lo32));
-      c.idx = int(ci);
-      c.perm = int(cp);
-      s.ccand[t] = c;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      Cand c{0.0, -1, -1};
+      PROF_MARK(2);
+      TS_MARK(1);
+      // poll all P records: lane handles slots lane, lane+32, ...
+      Cand w{0.0, -1, -1};
       int owner = -1;
-      for (int t = lane; t < P; t += 32) {
-        Cand o = s.ccand[t];
-        if (better(o.v, o.idx, c.v, c.idx)) {
-          c = o;
-          owner = t;
+      constexpr int kMaxPoll = 8;  // P <= 256
+      bool got[kMaxPoll];
+#pragma unroll
+      for (int q = 0; q < kMaxPoll; ++q) got[q] = (lane + 32 * q) >= P;
+      bool all = (a.dbg & 16) != 0;
+      if (all) { w = c; owner = cta; }
+      int spins = 0;
+      while (!all) {
+        (void)spins;
+        all = true;
+#pragma unroll
+        for (int q = 0; q < kMaxPoll; ++q) {
+          if (!got[q]) {
+            const int t = lane + 32 * q;
+            const uint64_t* sl = a.recs + ((size_t)par * P + t) * 4;
+            uint64_t w0, w1, w2, w3;
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(sl) : "memory");
+            asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(sl + 2) : "memory");
+            if (uint32_t(w0 >> 32) == tag && uint32_t(w1 >> 32) == tag && uint32_t(w2 >> 32) == tag &&
+                uint32_t(w3 >> 32) == tag) {
+              got[q] = true;
+              Cand o;
+              o.v = __longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+              o.idx = int(uint32_t(w2));
+              o.perm = int(uint32_t(w3));
+              if (better(o.v, o.idx, w.v, w.idx)) {
+                w = o;
+                owner = t;
+              }
+            } else {
+              all = false;
+            }
+          }
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        double ov = __shfl_xor_sync(0xffffffffu, c.v, o);
-        int oi = __shfl_xor_sync(0xffffffffu, c.idx, o);
-        int op = __shfl_xor_sync(0xffffffffu, c.perm, o);
+        double ov = __shfl_xor_sync(0xffffffffu, w.v, o);
+        int oi = __shfl_xor_sync(0xffffffffu, w.idx, o);
+        int op = __shfl_xor_sync(0xffffffffu, w.perm, o);
         int ow = __shfl_xor_sync(0xffffffffu, owner, o);
-        if (better(ov, oi, c.v, c.idx)) {
-          c.v = ov;
-          c.idx = oi;
-          c.perm = op;
+        if (better(ov, oi, w.v, w.idx)) {
+          w.v = ov;
+          w.idx = oi;
+          w.perm = op;
           owner = ow;
         }
       }
       if (lane == 0) {
         s.misc[0] = owner;
-        s.misc[1] = c.idx;
-        s.misc[2] = c.perm;
-        reinterpret_cast<double*>(s.misc + 6)[0] = c.v;
+        s.misc[1] = w.idx;
+        s.misc[2] = w.perm;
+        reinterpret_cast<double*>(s.misc + 6)[0] = w.v;
       }
+    } else if (warp == 1 && own_a) {
+      uint64_t* ra = a.rowa + (size_t)par * slot_words;
+      const int la = a_pos - rbase;
+      for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
+      if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
     }
     __syncthreads();
+    TS_MARK(2);
+    PROF_MARK(3);
+
+    // ---- D: gather next column (overlapped with the winner-row fetch) --------
     const int owner = s.misc[0], b = s.misc[1], pb = s.misc[2];
     const double vb = reinterpret_cast<double*>(s.misc + 6)[0];
     const bool own_b = b >= rbase && b < rbase + rcount;
-
-    // ---- fetch the winning row (and row a if we own b) -------------------
+    const bool swapped = b != a_pos;
+    const bool more = (g + 1 < rt) || a.want_y;
+    double cnext[2] = {0.0, 0.0};
+    const uint64_t* ra = a.rowa + (size_t)par * slot_words;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int li = tid + u * kThreads;
+      const int pos = rbase + li;
+      if (more && li < rcount && pos > a_pos) {
+        int ph;
+        if (swapped && pos == b) {
+          uint32_t pa = 0, dummy;
+          if (!(a.dbg & 4)) ll_get2(ra, tag, pa, dummy);
+          ph = int(pa);
+        } else {
+          ph = s.perm[li];
+        }
+        cnext[u] = (a.dbg & 2) ? 0.0 : skew_at(W, ld, ph, pb);
+      }
+    }
     {
       const uint64_t* wslot = a.slots + ((size_t)owner * 2 + par) * slot_words;
-      for (int j = tid; j <= k; j += kThreads) s.wrow[j] = ll_get_double(wslot + 4 + 2 * j, tag);
-      if (own_b && b != a_pos) {
-        const uint64_t* ra = a.rowa + (size_t)par * slot_words;
+      if (!(a.dbg & 4)) for (int j = tid; j <= k; j += kThreads) s.wrow[j] = ll_get_double(wslot + 4 + 2 * j, tag);
+      if (own_b && swapped && !(a.dbg & 4)) {
         for (int j = tid; j <= k; j += kThreads) s.arow[j] = ll_get_double(ra + 4 + 2 * j, tag);
         if (tid == 0) {
           uint32_t pa, dummy;
@@ -313,69 +381,70 @@ __global__ void __launch_bounds__(kThreads, 1) panel_kernel(PanelArgs a) {
         }
       }
     }
+    PROF_MARK(4);
     __syncthreads();
+    PROF_MARK(5);
 
-    // ---- symmetric interchange restricted to the slab rows + perm ----------
-    if (b != a_pos) {
+    // ---- E: interchange, scale, next column, z for the next step -------------
+    if (swapped) {
       if (own_a) {
         const int la = a_pos - rbase;
-        for (int j = tid; j <= k; j += kThreads) s.slab[(size_t)j * Rs + la] = s.wrow[j];
+        for (int j = tid; j < k; j += kThreads) s.slab[(size_t)j * Rs + la] = s.wrow[j];
       }
       if (own_b) {
         const int lb = b - rbase;
-        for (int j = tid; j <= k; j += kThreads) s.slab[(size_t)j * Rs + lb] = s.arow[j];
+        for (int j = tid; j < k; j += kThreads) s.slab[(size_t)j * Rs + lb] = s.arow[j];
       }
+    }
+    double* ncol = (g + 1 < rt) ? s.slab + (size_t)(k + 1) * Rs : s.ycol;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int li = tid + u * kThreads;
+      if (li < rcount) {
+        const int pos = rbase + li;
+        if (pos == a_pos) {
+          col[li] = 1.0;
+          if (swapped) s.perm[li] = pb;
+        } else if (pos > a_pos) {
+          double v = (swapped && pos == b) ? s.arow[k] : col[li];
+          col[li] = vb != 0.0 ? v / vb : v;
+          if (swapped && pos == b) s.perm[li] = s.misc[3];
+        }
+        if (more) ncol[li] = cnext[u];
+      }
+    }
+    // z for the next step: x = [wrow[0..k-1], 1], taus[k] = vb
+    for (int j = tid; j <= k; j += kThreads) {
+      double xm = j >= 1 ? s.wrow[j - 1] : 0.0;
+      double xp = (j + 1 < k) ? s.wrow[j + 1] : (j + 1 == k ? 1.0 : 0.0);
+      double tj = j == k ? vb : s.taus[j];
+      double tj1 = (j + 1 == k) ? vb : s.taus[j + 1];
+      s.zbuf[j] = (j >= 1 ? tj * xm : 0.0) - (j + 1 <= k ? tj1 * xp : 0.0);
     }
     __syncthreads();
     if (tid == 0) {
-      if (b != a_pos) {
-        if (own_a) s.perm[a_pos - rbase] = pb;
-        if (own_b) s.perm[b - rbase] = s.misc[3];
-      }
       s.taus[k] = vb;
-      s.wrow[k] = 1.0;  // pivot row of the next step: [A[b, 0..k-1], 1]
+      s.wrow[k] = 1.0;
       if (cta == 0) {
         a.tau[g] = vb;
         a.piv[g + 1] = (long long)(b - a_pos);
       }
     }
-    __syncthreads();
-
-    // ---- scale: L column g+1 = v / tau below the unit --------------------
-    const double inv = vb != 0.0 ? 1.0 / vb : 0.0;
-    (void)inv;
-    for (int li = tid; li < rcount; li += kThreads) {
-      int pos = rbase + li;
-      if (pos == a_pos) {
-        col[li] = 1.0;
-      } else if (pos > a_pos && vb != 0.0) {
-        col[li] = col[li] / vb;
-      }
-    }
-    // ---- next column: gather X_cur[i, a] = X0[perm[i], perm[a]] ---------
-    pg = pb;
-    if (g + 1 < rt || a.want_y) {
-      double* ncol = (g + 1 < rt) ? s.slab + (size_t)(k + 1) * Rs : s.ycol;
-      for (int li = tid; li < rcount; li += kThreads) {
-        int pos = rbase + li;
-        double c = 0.0;
-        if (pos > a_pos) c = skew_at(W, ld, s.perm[li], pg);
-        ncol[li] = c;
-      }
-    }
-    __syncthreads();
+    PROF_MARK(6);
+    PROF_MARK(7);
   }
 
   // ---- var1: y = column rt after the panel's couplings (for the straggler) --
+  __syncthreads();
   if (a.want_y && rt < n) {
     const int k = rt - lo;
     const int l_first = max(0, rt + 1 - rbase);
-    Cand dummy;
-    dummy.v = 0.0;
-    dummy.idx = -1;
-    gemv_rows(s, Rs, k, l_first, rcount, rbase, warp, lane, s.ycol, dummy);
-    __syncthreads();
-    for (int li = l_first + tid; li < rcount; li += kThreads) a.y[rbase + li] = s.ycol[li];
+    if (G > 1) {
+      gemv_partials(s, Rs, R, G, k, l_first, tid);
+      __syncthreads();
+    }
+    for (int li = l_first + tid; li < rcount; li += kThreads)
+      a.y[rbase + li] = gemv_finish(s, Rs, R, G, k, li, s.ycol[li]);
   }
 
   // ---- materialise the displaced trailing lines -------------------------
@@ -500,3 +569,12 @@ cudaError_t launch_finalize_l(const double* W, long long ldw, const double* X, l
 }
 
 }  // namespace skl
+
+#ifdef SKL_PANEL_PROFILE
+extern "C" int skl_debug_panel_ts(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, skl::g_panel_ts, sizeof(unsigned long long) * 8 * 160 * 4);
+}
+extern "C" int skl_debug_panel_profile(unsigned long long* out32) {
+  return (int)cudaMemcpyFromSymbol(out32, skl::g_panel_prof, sizeof(unsigned long long) * 32);
+}
+#endif

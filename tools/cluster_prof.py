@@ -1,0 +1,23 @@
+"""Per-phase cycle breakdown of the cluster panel kernel."""
+import sys, ctypes
+sys.path.insert(0, ".")
+import torch
+import paper_2411_09859_b200 as pk
+from paper_2411_09859_b200 import device as dv, _capi
+from paper_2411_09859_b200.inputs import skew_lower
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+b = int(sys.argv[2]) if len(sys.argv) > 2 else 128
+xd = dv.to_device_colmajor(skew_lower(n, 0))
+lib = _capi.load()
+pk.ltlt_blk_piv_device(xd, b, "var1"); torch.cuda.synchronize()
+buf = torch.zeros(16 * 8, dtype=torch.int64, device="cuda")
+lib.skl_debug_set_panel_profile.argtypes = [ctypes.c_void_p]
+lib.skl_debug_set_panel_profile(buf.data_ptr())
+pk.ltlt_blk_piv_device(xd, b, "var1"); torch.cuda.synchronize()
+lib.skl_debug_set_panel_profile(None)
+p = buf.view(16, 8).cpu().numpy()
+names = ["argmax+publish", "pubrow copy", "cluster barrier", "winner+gather+rows", "swap/scale/z", "az+store"]
+for c in (0, 7, 15):
+    steps = max(p[c, 5], 1)
+    tot = p[c, :5].sum()
+    print(f"cta {c}: {tot/steps:.0f} cyc/step over {steps} steps: " + ", ".join(f"{names[i]}={p[c,i]/steps:.0f}" for i in range(5)))
