@@ -1,11 +1,6 @@
 // Temporary placeholders (replaced by twostep.cu / batched.cu).
 #include "internal.h"
 namespace skl {
-size_t twostep_workspace_bytes(int n) { return (size_t)n * n * sizeof(double) + 4096; }
-cudaError_t launch_twostep(const double*, long long, double*, long long, int, int, double*, long long*, int*, void*,
-                           cudaStream_t) {
-  return cudaErrorNotSupported;
-}
 template <typename T>
 cudaError_t launch_batched(int, int, const T*, long long, long long, T*, long long, long long, T*, long long,
                            long long*, long long, double*, double*, cudaStream_t) {
