@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 pivoted LTL^T hot path (driver contract).
+
+Workload (BASELINE.json configs[1]): blocked fp64 pivoted LTL^T of one
+n=4096 skew matrix X = G - G^T (G iid N(0,1), Philox seed 0), block nb=128,
+reference default trailing scheme var1.  A "step" is one factorization.
+Metric: LTL^T factorization GFLOP/s with the reference's n^3/3 flop model
+(cli.py:146, oracle.py:164-172), plus the config-2 skr2k microbench
+(C 4096^2 lower -= W B^T - B W^T, keff = 64) in GFLOP/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Multi-GPU: one matrix does not shard across GPUs on this path (DESIGN.md,
+"replicas only"), so N ranks factor N independent matrices (weak scaling);
+value = all ranks' flops / max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N, NB, FUSED = 4096, 128, "var1"
+FLOPS = N ** 3 / 3.0                       # n^3/3 (reference normalisation)
+SKR2K_FLOPS = 4 * 64 * (N * (N - 1) // 2)  # kernels3.py:323 with keff = 64
+METRIC = "LTL^T factorization GFLOP/s (n^3/3) and % of FP64 peak; skr2k GFLOP/s"
+
+
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(world, v):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def fp64_gemm_peak(torch):
+    """cuBLAS DGEMM 8192^3 burst (library GEMM as the FP64 tensor-pipe yardstick)."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e30
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(3):
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def cpu_baseline_port(x, budget_s=30.0):
+    """The oracle (NumPy restatement of the reference) on the host cores."""
+    import oracle
+    t0 = time.perf_counter()
+    oracle.ltlt_blk_piv(x, b=NB, fused=FUSED)
+    dt = time.perf_counter() - t0
+    reps = 1
+    return FLOPS / dt / 1e9, reps, dt
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm on the host CPU (the oracle port
+    of the pure-Python reference, numpy + OpenBLAS on all host threads)."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2411_09859_b200.inputs import skew_lower
+    x = skew_lower(N, 0)
+    cores = os.cpu_count() or 1
+    t_w = []
+    for _ in range(args.warmup):
+        t0 = time.perf_counter()
+        oracle.ltlt_blk_piv(x, b=NB, fused=FUSED)
+        t_w.append(time.perf_counter() - t0)
+        if sum(t_w) > 60:
+            break
+    est = t_w[-1] if t_w else 10.0
+    steps = max(1, min(args.steps, int(150.0 / max(est, 1e-3))))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.ltlt_blk_piv(x, b=NB, fused=FUSED)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    val = FLOPS / (ms * 1e-3) / 1e9
+    sample = (f"{len(times)} full factorizations of config 2 (n={N}, nb={NB}, {FUSED}); "
+              f"{len(t_w)} warm-up; OpenBLAS threads={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}")
+    line = {"metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "impl": "reference", "n_gpus": 0,
+            "steps": len(times), "warmup": len(t_w), "ms_per_step": round(ms, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"blocked pivoted LTL^T n={N} nb={NB} {FUSED}", "n": N, "nb": NB,
+                       "fused": FUSED, "input": "X=G-G^T, G~N(0,1) Philox seed 0"},
+            "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import paper_2411_09859_b200 as pk
+    from paper_2411_09859_b200 import _capi
+    from paper_2411_09859_b200 import device as dv
+    from paper_2411_09859_b200.inputs import skew_lower
+    from paper_2411_09859_b200.instrument import flops_blk_piv
+
+    torch.cuda.set_device(local)
+    lib = _capi.load()
+    x = skew_lower(N, rank)  # each replica factors its own matrix (rank 0: the config's seed 0)
+    x_pin = torch.empty((N, N), dtype=torch.float64).pin_memory()
+    x_pin.copy_(torch.from_numpy(np.ascontiguousarray(x.T)))  # (cols, rows) row-major == column-major X
+    xd = x_pin.to("cuda").t()
+    L = dv.empty_colmajor(N, N, torch.float64)
+    tau = torch.empty(N - 1, dtype=torch.float64, device="cuda")
+    piv = torch.empty(N, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    for _ in range(args.warmup):
+        pk.ltlt_blk_piv_device(xd, NB, FUSED, out=(L, tau, piv))
+    torch.cuda.synchronize()
+
+    # ---- device-resident timing (L2 flushed between steps, outside the events) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    lib.skl_timing_enable(0)
+    l0 = lib.skl_launch_count()
+    step_ms = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record()
+        pk.ltlt_blk_piv_device(xd, NB, FUSED, out=(L, tau, piv))
+        e1.record()
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    barrier(world)
+    launches = int(lib.skl_launch_count() - l0)
+    clocks = sampler.stop()
+    ms = max_over_ranks(world, sum(step_ms) / len(step_ms))
+    value = world * FLOPS / (ms * 1e-3) / 1e9
+
+    # ---- end to end: pinned H2D of X, factorize, D2H of L, tau, piv ---------------
+    L_pin = torch.empty((N, N), dtype=torch.float64).pin_memory()
+    tau_pin = torch.empty(N - 1, dtype=torch.float64).pin_memory()
+    piv_pin = torch.empty(N, dtype=torch.int64).pin_memory()
+    xcols = torch.empty((N, N), dtype=torch.float64, device="cuda")
+    e2e_ms = []
+    for _ in range(max(2, args.steps // 2)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record()
+        xcols.copy_(x_pin, non_blocking=True)
+        pk.ltlt_blk_piv_device(xcols.t(), NB, FUSED, out=(L, tau, piv))
+        L_pin.copy_(L.t(), non_blocking=True)
+        tau_pin.copy_(tau, non_blocking=True)
+        piv_pin.copy_(piv, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e = max_over_ranks(world, sum(e2e_ms) / len(e2e_ms))
+    e2e_value = world * FLOPS / (e2e * 1e-3) / 1e9
+
+    # ---- per-kernel-class times (roofline of the dominant kernel) -----------------
+    lib.skl_timing_enable(1)
+    prof_runs = 2
+    for _ in range(prof_runs):
+        flush.zero_()
+        pk.ltlt_blk_piv_device(xd, NB, FUSED, out=(L, tau, piv))
+    torch.cuda.synchronize()
+    import ctypes
+    kms = (ctypes.c_double * 4)()
+    kcnt = (ctypes.c_int * 4)()
+    lib.skl_timing_read(kms, kcnt)
+    lib.skl_timing_enable(0)
+    kinds = ["panel", "pack", "trailing_gemm", "finalize"]
+    per_fact = {kinds[i]: kms[i] / prof_runs for i in range(4)}
+    cnt = {kinds[i]: kcnt[i] // prof_runs for i in range(4)}
+    piv_h, tau_h = piv.cpu().numpy(), tau.cpu().numpy()
+    fc = flops_blk_piv(N, NB, FUSED, piv_h, tau_h)
+    hbm_peak, peak_src = measured_peaks()
+    fp64_peak = fp64_gemm_peak(torch)
+    dominant = max(per_fact, key=per_fact.get)
+    if dominant == "trailing_gemm":
+        ach = fc.level3 / cnt[dominant] / (per_fact[dominant] / cnt[dominant] * 1e-3) / 1e12
+        roof = {"kernel": "gemm_lower_nt_kernel (DMMA)", "bound": "tensor", "achieved": round(ach, 3),
+                "peak": round(fp64_peak, 3), "unit": "TFLOP/s", "frac": round(ach / fp64_peak, 4),
+                "traffic": None, "peak_source": "cuBLAS DGEMM 8192^3 measured live"}
+    else:
+        # level-2 algorithmic bytes: 4 B per counted panel flop + 16 B per moved element
+        alg_bytes = 4 * fc.panel + 16 * fc.pivot
+        per_launch_bytes = alg_bytes / cnt["panel"]
+        per_launch_s = per_fact["panel"] / cnt["panel"] * 1e-3
+        ach = per_launch_bytes / per_launch_s / 1e9
+        roof = {"kernel": "panel_cluster_kernel (pivoted left-looking panel)", "bound": "hbm",
+                "achieved": round(ach, 2), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
+                "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": int(per_launch_bytes), "launches_per_step": cnt["panel"]}
+    gemm_tf = fc.level3 / (per_fact["trailing_gemm"] * 1e-3) / 1e12 if per_fact["trailing_gemm"] else None
+
+    # ---- skr2k microbench (config 2b): C(4096^2 lower) += W B^T - B W^T -----------
+    from paper_2411_09859_b200 import kernels3
+    rng = np.random.default_rng(0)
+    Bh = rng.standard_normal((N, 128))
+    Bd = dv.to_device_colmajor(Bh)
+    taud = torch.as_tensor(rng.standard_normal(127), device="cuda")
+    Wd = kernels3.form_w_device(Bd, taud)
+    Cd = dv.to_device_colmajor(rng.standard_normal((N, N)))
+    nbytes = lib.skl_skr2k_workspace_size(N, 128)
+    ws = dv.workspace(nbytes)
+    skr_ms = []
+    for it in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0.record()
+        st = lib.skl_skr2k_lower(N, 128, 1.0, Bd.data_ptr(), N, Wd.data_ptr(), N, 1.0, Cd.data_ptr(), N, 1,
+                                 ws.data_ptr(), nbytes, None, dv.stream_ptr())
+        e1.record()
+        torch.cuda.synchronize()
+        _capi.check(st, "skr2k")
+        if it >= args.warmup:
+            skr_ms.append(e0.elapsed_time(e1))
+    skr = SKR2K_FLOPS / (statistics.median(skr_ms) * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"blocked pivoted LTL^T n={N} nb={NB} {FUSED} (BASELINE configs[1])", "n": N,
+                   "nb": NB, "fused": FUSED, "input": "X=G-G^T, G~N(0,1) Philox seed rank",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "pct_fp64_peak": round(100 * value / world / 1e3 / fp64_peak, 2),
+        "fp64_peak_tflops": round(fp64_peak, 2),
+        "skr2k": {"value": round(skr, 1), "unit": "GFLOP/s", "flops": SKR2K_FLOPS,
+                  "pct_fp64_peak": round(100 * skr / 1e3 / fp64_peak, 2)},
+        "kernels_ms_per_step": {k: round(v, 4) for k, v in per_fact.items()},
+        "trailing_gemm_tflops": round(gemm_tf, 2) if gemm_tf else None,
+        "roofline": roof,
+        "e2e": {"value": round(e2e_value, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": N * N * 8,
+                "d2h_bytes_per_step": N * N * 8 + (N - 1) * 8 + N * 8, "ms_per_step": round(e2e, 4)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, reps, dt = cpu_baseline_port(x)
+        line["cpu_baseline"] = {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"{reps} full factorization of config 2 by the oracle port ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,17 @@ int skl_ltlt_batched_piv(int batch, int n, int dtype, const void* X, long long l
                          long long ldl, long long strideL, void* tau, long long* piv, double* pf_sign,
                          double* pf_logabs, void* stream);
 
+/* ---- instrumentation (bench / profiling) ---------------------------------
+ * skl_timing_enable(1) records CUDA events around every kernel the blocked
+ * driver launches, by class (0 panel, 1 operand pack, 2 trailing GEMM,
+ * 3 finalize); skl_timing_read() returns total ms and launch counts per class
+ * after the caller synchronised the stream.  skl_launch_count() counts
+ * library kernel launches since the last skl_timing_enable().               */
+int skl_timing_enable(int on);
+int skl_timing_read(double* ms4, int* count4);
+long long skl_launch_count(void);
+int skl_debug_set_panel_profile(unsigned long long* dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,10 @@ SIGNATURES = {
     "skl_ltlt_unb_twostep_workspace_size": (_sz, [_i]),
     "skl_ltlt_unb_twostep": (_i, [_i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
     "skl_ltlt_batched_piv": (_i, [_i, _i, _i, _p, _ll, _ll, _p, _ll, _ll, _p, _p, _p, _p, _p]),
+    "skl_timing_enable": (_i, [_i]),
+    "skl_timing_read": (_i, [_p, _p]),
+    "skl_launch_count": (_ll, []),
+    "skl_debug_set_panel_profile": (_i, [_p]),
 }
 
 

@@ -21,6 +21,35 @@ namespace {
 thread_local std::string g_last_error;
 unsigned long long* g_prof = nullptr;  // debug: panel phase profile (device)
 
+// ---- optional per-kernel-class timing of the blocked driver (CUDA events on
+// the launching stream; bench.py uses it for the roofline of the top kernel)
+enum { KPANEL = 0, KPACK = 1, KGEMM = 2, KFINAL = 3, KNUM = 4 };
+struct KTimer {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[KNUM];
+  long long launches = 0;
+} g_kt;
+
+struct KScope {
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t b = nullptr, e = nullptr;
+  KScope(int k, cudaStream_t s) : kind(k), st(s) {
+    g_kt.launches++;
+    if (g_kt.on) {
+      cudaEventCreate(&b);
+      cudaEventCreate(&e);
+      cudaEventRecord(b, st);
+    }
+  }
+  ~KScope() {
+    if (g_kt.on) {
+      cudaEventRecord(e, st);
+      g_kt.ev[kind].push_back({b, e});
+    }
+  }
+};
+
 int fail_cuda(cudaError_t e, const char* where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
   return SKL_CUDA_ERROR;
@@ -205,6 +234,37 @@ extern "C" {
 const char* skl_version(void) { return "skewltl_b200 0.1.0 (sm_100a)"; }
 const char* skl_last_error(void) { return g_last_error.c_str(); }
 
+// per-kernel-class timing: enable/disable (clears), read after the stream has synced
+int skl_timing_enable(int on) {
+  for (auto& v : g_kt.ev)
+    for (auto& p : v) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
+  for (auto& v : g_kt.ev) v.clear();
+  g_kt.on = on != 0;
+  g_kt.launches = 0;
+  return SKL_OK;
+}
+
+// ms[k] = total milliseconds of kernel class k (panel, pack, gemm, finalize); cnt[k] = launches
+int skl_timing_read(double* ms, int* cnt) {
+  for (int k = 0; k < KNUM; ++k) {
+    double tot = 0.0;
+    for (auto& p : g_kt.ev[k]) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, p.first, p.second) != cudaSuccess) return fail_cuda(cudaGetLastError(), "timing");
+      tot += t;
+    }
+    ms[k] = tot;
+    cnt[k] = (int)g_kt.ev[k].size();
+  }
+  return SKL_OK;
+}
+
+// number of kernel launches issued by the library since the last skl_timing_enable()
+long long skl_launch_count(void) { return g_kt.launches; }
+
 // debug hook: route per-CTA panel phase cycle counters to a device buffer (NULL disables)
 int skl_debug_set_panel_profile(unsigned long long* dev_buf) {
   g_prof = dev_buf;
@@ -237,11 +297,18 @@ int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, 
   double* Q = b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
   int* keep = b.take<int>(std::max(k, 1));
   int* cnt = b.take<int>(4);  // [0] keff, [1] nk4
-  if (n <= 1) {
-    if (keff_dev) SKL_TRY(cudaMemsetAsync(keff_dev, 0, sizeof(int), st));
-    return SKL_OK;
-  }
-  if (k == 0 || alpha == 0.0) {
+  if (n <= 1 || k == 0 || alpha == 0.0) {
+    if (n <= 1) {
+      if (keff_dev) {
+        if (k == 0 || n <= 0) {
+          SKL_TRY(cudaMemsetAsync(keff_dev, 0, sizeof(int), st));
+        } else {
+          SKL_TRY(skl::launch_rank2k_keep(A, lda, B, ldb, n, k, skip_zero_cols, keep, cnt, cnt + 1, st));
+          SKL_TRY(cudaMemcpyAsync(keff_dev, cnt, sizeof(int), cudaMemcpyDeviceToDevice, st));
+        }
+      }
+      return SKL_OK;
+    }
     SKL_TRY(skl::launch_scale_lower<double>(C, ldc, n, beta, st));
     if (keff_dev) {
       if (k == 0) {
@@ -253,6 +320,7 @@ int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, 
     }
     return SKL_OK;
   }
+  g_kt.launches += 3;
   SKL_TRY(skl::launch_rank2k_keep(A, lda, B, ldb, n, k, skip_zero_cols, keep, cnt, cnt + 1, st));
   SKL_TRY(skl::launch_pack_rank2k(A, lda, B, ldb, n, k, alpha, keep, cnt, k4cap, P, Q, st));
   SKL_TRY(skl::launch_gemm_lower(P, Q, k4cap, k4cap, cnt + 1, C, ldc, n, beta, st));
@@ -410,10 +478,13 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     static int dbg = env_int("SKL_PANEL_DBG", 0);
     a.dbg = dbg;
     a.prof = g_prof;
-    if (p.cluster)
-      SKL_TRY(skl::launch_panel_cluster(a, st));
-    else
-      SKL_TRY(skl::launch_panel(a, st));
+    {
+      KScope ks(KPANEL, st);
+      if (p.cluster)
+        SKL_TRY(skl::launch_panel_cluster(a, st));
+      else
+        SKL_TRY(skl::launch_panel(a, st));
+    }
     tag += (uint32_t)p.nelim + 1;
 
     const int ntr = n - rt;
@@ -421,14 +492,24 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
       const int ka = rt - p.lo;
       const int K = ka + (straggler ? 2 : 0);
       const int nk4 = (K + 3) / 4;
-      SKL_TRY(skl::launch_pack_rankk(ws.W + (size_t)p.lo * ld + rt, ld, ntr, ka, tau + p.lo + 1, -1.0,
-                                     straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st));
-      SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, ws.W + (size_t)rt * ld + rt, ld, ntr, 1.0,
-                                     st));
+      {
+        KScope ks(KPACK, st);
+        SKL_TRY(skl::launch_pack_rankk(ws.W + (size_t)p.lo * ld + rt, ld, ntr, ka, tau + p.lo + 1, -1.0,
+                                       straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st));
+      }
+      {
+        KScope ks(KGEMM, st);
+        SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, ws.W + (size_t)rt * ld + rt, ld, ntr,
+                                       1.0, st));
+      }
     }
   }
-  SKL_TRY(skl::launch_compose_suffix(ws.gperm_all, (int)plan.size(), nullptr, n, ws.sigma_all, st));
-  SKL_TRY(skl::launch_finalize_l(ws.W, ld, X, ldx, L, ldl, n, ws.col_group, ws.sigma_all, L != X ? 1 : 0, st));
+  {
+    KScope ks(KFINAL, st);
+    SKL_TRY(skl::launch_compose_suffix(ws.gperm_all, (int)plan.size(), nullptr, n, ws.sigma_all, st));
+    g_kt.launches++;
+    SKL_TRY(skl::launch_finalize_l(ws.W, ld, X, ldx, L, ldl, n, ws.col_group, ws.sigma_all, L != X ? 1 : 0, st));
+  }
   return SKL_OK;
 }
 
@@ -439,6 +520,7 @@ int skl_ltlt_unb_twostep(int n, int pivot, const double* X, long long ldx, doubl
                          long long* piv, int* info_dev, void* workspace, size_t workspace_bytes, void* stream) {
   if (n < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
   if (workspace_bytes < skl::twostep_workspace_bytes(n)) return SKL_BAD_ARGUMENT;
+  g_kt.launches += (L != X) ? 2 : 1;
   SKL_TRY(skl::launch_twostep(X, ldx, L, ldl, n, pivot, tau, piv, info_dev, workspace,
                               static_cast<cudaStream_t>(stream)));
   return SKL_OK;

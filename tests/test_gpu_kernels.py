@@ -1,0 +1,144 @@
+"""GPU parity of the stand-alone kernels (kernels2/kernels3/core API) vs the oracle."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import lower
+
+pytestmark = pytest.mark.gpu
+RNG = np.random.default_rng(2024)
+
+
+def k3():
+    from paper_2411_09859_b200 import kernels3
+    return kernels3
+
+
+def k2():
+    from paper_2411_09859_b200 import kernels2
+    return kernels2
+
+
+@pytest.mark.parametrize("n,k", [(1, 3), (2, 2), (37, 5), (300, 10), (513, 129), (1000, 64)])
+@pytest.mark.parametrize("alpha,beta", [(1.0, 1.0), (-0.5, 2.0), (1.0, 0.0)])
+def test_skew_rank2k(n, k, alpha, beta):
+    a = RNG.standard_normal((n, k))
+    w = oracle.form_w(a, RNG.standard_normal(max(k - 1, 0)))
+    c = np.asfortranarray(RNG.standard_normal((n, n)))
+    want = c.copy()
+    keff = oracle.skew_rank2k(want, alpha, a, w) if beta == 1.0 else None
+    if beta != 1.0:
+        want = beta * c
+        keff = oracle.skew_rank2k(want, alpha, a, w)
+        want = np.where(np.tril(np.ones((n, n), bool), -1), want, c)
+    got = c.copy()
+    k3().skew_rank2k(got, alpha, a, w, beta)
+    low = np.tril(np.ones((n, n), bool), -1)
+    assert np.allclose(got[low], want[low], rtol=1e-12, atol=1e-12 * max(k, 1))
+    assert np.array_equal(got[~low], c[~low])
+    assert k3().last_keff == keff
+
+
+def test_skew_rank2k_config2_microbench_shape():
+    n, k = 4096, 128
+    a = RNG.standard_normal((n, k))
+    w = oracle.form_w(a, RNG.standard_normal(k - 1))
+    c = np.asfortranarray(RNG.standard_normal((n, n)))
+    want = c.copy()
+    oracle.skew_rank2k(want, 1.0, a, w)
+    got = c.copy()
+    k3().skew_rank2k(got, 1.0, a, w, 1.0)
+    assert k3().last_keff == 64
+    low = np.tril(np.ones((n, n), bool), -1)
+    assert np.max(np.abs(got[low] - want[low])) <= 1e-13 * k * np.max(np.abs(want[low]))
+
+
+def test_skew_rank2k_alias_and_shape_errors():
+    a = RNG.standard_normal((6, 6))
+    with pytest.raises(ValueError):
+        k3().skew_rank2k(a, 1.0, a, a.copy())
+    with pytest.raises(ValueError):
+        k3().skew_rank2k(np.zeros((5, 5)), 1.0, np.zeros((5, 2)), np.zeros((5, 3)))
+
+
+@pytest.mark.parametrize("n,k", [(2, 1), (50, 4), (400, 129), (777, 256)])
+def test_skew_tridiag_rankk(n, k):
+    from paper_2411_09859_b200.core import SkewTridiagonal
+    a = RNG.standard_normal((n, k))
+    tau = RNG.standard_normal(k - 1)
+    c = np.asfortranarray(RNG.standard_normal((n, n)))
+    want = c.copy()
+    oracle.skew_tridiag_rankk(want, -1.0, a, tau)
+    got = c.copy()
+    k3().skew_tridiag_rankk(got, -1.0, a, SkewTridiagonal(tau))
+    low = np.tril(np.ones((n, n), bool), -1)
+    assert np.allclose(got[low], want[low], rtol=1e-12, atol=1e-12 * k)
+    assert np.array_equal(got[~low], c[~low])
+
+
+@pytest.mark.parametrize("n,k", [(5, 2), (9, 7), (300, 128)])
+def test_form_w_bit_exact(n, k):
+    from paper_2411_09859_b200.core import SkewTridiagonal, form_s_splitting
+    a = RNG.standard_normal((n, k))
+    tau = RNG.standard_normal(k - 1)
+    w = k3().form_w(a, form_s_splitting(SkewTridiagonal(tau)))
+    assert np.array_equal(w, oracle.form_w(a, tau))
+
+
+@pytest.mark.parametrize("n", [2, 3, 16, 64, 300])
+def test_skew_rank2(n):
+    a = np.asfortranarray(RNG.standard_normal((n, n)))
+    x, y = RNG.standard_normal(n), RNG.standard_normal(n)
+    want = 0.5 * lower(a) + 1.25 * lower(np.outer(x, y) - np.outer(y, x))
+    got = a.copy()
+    k2().skew_rank2(got, 1.25, x, y, 0.5)
+    assert np.allclose(lower(got), want, rtol=1e-14, atol=1e-14)
+    assert np.array_equal(np.triu(got), np.triu(a))
+    two = np.zeros((2, 2), order="F")
+    k2().skew_rank2(two, 1.0, np.array([1.0, 0.0]), np.array([0.0, 1.0]), 1.0)
+    assert two[1, 0] == -1.0
+
+
+def test_skew_tridiag_gemv():
+    from paper_2411_09859_b200.core import SkewTridiagonal
+    y = np.zeros(3)
+    k2().skew_tridiag_gemv(y, 1.0, np.eye(3), SkewTridiagonal(np.array([2.0, 3.0])), np.ones(3), 0.0)
+    assert y.tolist() == [-2.0, -1.0, 3.0]
+    p, k = 40, 9
+    a = RNG.standard_normal((p, k))
+    tau, x = RNG.standard_normal(k - 1), RNG.standard_normal(k)
+    y0 = RNG.standard_normal(p - 5)
+    want = y0.copy()
+    oracle.skew_tridiag_gemv(want, -1.0, a, tau, x, tail_from=5)
+    got = y0.copy()
+    k2().skew_tridiag_gemv(got, -1.0, a, SkewTridiagonal(tau), x, tail_from=5)
+    assert np.allclose(got, want, rtol=1e-14, atol=1e-14)
+
+
+@pytest.mark.parametrize("forward", [True, False])
+def test_apply_row_pivots_bit_exact(forward):
+    n, q = 60, 17
+    piv = np.zeros(n, dtype=np.int64)
+    for k in range(n):
+        piv[k] = RNG.integers(0, n - k)
+    block = np.asfortranarray(RNG.standard_normal((n, q)))
+    want = block.copy()
+    oracle.apply_row_pivots(want, piv, forward)
+    got = block.copy()
+    k2().apply_row_pivots(got, piv, forward)
+    assert np.array_equal(got, want)
+
+
+def test_apply_symmetric_pivot_bit_exact():
+    from paper_2411_09859_b200.core import SkewMatrixLower, apply_symmetric_pivot
+    n = 40
+    x = np.asfortranarray(np.tril(RNG.standard_normal((n, n)), -1))
+    for k, pi in [(0, 5), (3, 30), (10, 1), (38, 1), (7, 0)]:
+        want = x.copy()
+        oracle.sym_swap_lower(want, k, k + pi)
+        sx = SkewMatrixLower(x.copy(order="F"))
+        apply_symmetric_pivot(sx, k, pi)
+        assert np.array_equal(sx.data, want)
+    with pytest.raises(IndexError):
+        apply_symmetric_pivot(SkewMatrixLower(x), 35, 10)
