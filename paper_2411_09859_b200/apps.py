@@ -58,3 +58,72 @@ def pfaffian_slog(x: SkewMatrixLower, b=None):
     res = ltlt_blk_piv(x, b=b or min(DEFAULT_BLOCK, m))
     tau = res.t.tau.detach().cpu().numpy() if hasattr(res.t.tau, "detach") else res.t.tau
     return slog_from_factors(tau, res.p.pivots, m)
+
+
+def _batched_device(xd, dtype_code, stream=None):
+    from . import _capi
+    from . import device as dv
+    t = dv.require_cuda()
+    batch, n, _ = xd.shape
+    L = t.empty_like(xd)
+    tau = t.empty((batch, max(n - 1, 1)), dtype=xd.dtype, device=xd.device)
+    piv = t.empty((batch, n), dtype=t.int64, device=xd.device)
+    sign = t.empty(batch, dtype=t.float64, device=xd.device)
+    logabs = t.empty(batch, dtype=t.float64, device=xd.device)
+    st = _capi.load().skl_ltlt_batched_piv(batch, n, dtype_code, xd.data_ptr(), n, n * n, L.data_ptr(), n, n * n,
+                                          tau.data_ptr(), piv.data_ptr(), sign.data_ptr(), logabs.data_ptr(),
+                                          dv.stream_ptr(stream))
+    _capi.check(st, "ltlt_batched_piv")
+    return L, tau[:, : n - 1], piv, sign, logabs
+
+
+def ltlt_batched_piv_device(xd, stream=None):
+    """Device entry for many independent matrices.
+
+    ``xd``: CUDA tensor (batch, n, n), float64 or float32, with xd[b, j, i] =
+    X_b[i, j] (each matrix column-major, ld = n).  Returns device tensors
+    (L, tau, piv, sign, logabs) without synchronising; L has the layout of xd.
+    """
+    from . import _capi
+    from . import device as dv
+    t = dv.require_cuda()
+    if xd.dim() != 3 or xd.shape[1] != xd.shape[2] or not xd.is_contiguous():
+        raise ValueError("xd must be a contiguous (batch, n, n) CUDA tensor")
+    if xd.dtype == t.float64:
+        code = _capi.SKL_F64
+    elif xd.dtype == t.float32:
+        code = _capi.SKL_F32
+    else:
+        raise TypeError("batched factorization supports float64 and float32")
+    return _batched_device(xd, code, stream)
+
+
+def pfaffian_batched(xs):
+    """(sign, log|Pf|) of every matrix in ``xs`` ((batch, m, m) NumPy array of
+    lower-stored skew matrices, xs[b] indexed [row, col]); one launch.  The
+    per-matrix factorization is that of ``pfaffian`` (apps.py:12-30)."""
+    from . import device as dv
+    t = dv.require_cuda()
+    xs = np.asarray(xs)
+    if xs.ndim != 3 or xs.shape[1] != xs.shape[2]:
+        raise ValueError("xs must be (batch, m, m)")
+    if xs.dtype not in (np.float64, np.float32):
+        raise TypeError("float64 or float32 required")
+    m = xs.shape[1]
+    if m == 0:
+        return np.ones(xs.shape[0]), np.zeros(xs.shape[0])
+    xd = t.from_numpy(np.ascontiguousarray(np.swapaxes(xs, 1, 2))).to("cuda")
+    _L, _tau, _piv, sign, logabs = ltlt_batched_piv_device(xd)
+    return sign.cpu().numpy(), logabs.cpu().numpy()
+
+
+def ltlt_batched_piv(xs):
+    """Batched drop-in: per-matrix (L buffer, tau, pivots) as NumPy arrays plus
+    (sign, log|Pf|); each matrix's factors are those of ltlt_blk_piv(x_b, b=m)."""
+    from . import device as dv
+    t = dv.require_cuda()
+    xs = np.asarray(xs)
+    xd = t.from_numpy(np.ascontiguousarray(np.swapaxes(xs, 1, 2))).to("cuda")
+    L, tau, piv, sign, logabs = ltlt_batched_piv_device(xd)
+    Lh = np.swapaxes(L.cpu().numpy(), 1, 2)
+    return Lh, tau.cpu().numpy(), piv.cpu().numpy(), sign.cpu().numpy(), logabs.cpu().numpy()

@@ -1,0 +1,297 @@
+// Batched pivoted LTL^T + Pfaffian of many independent skew matrices
+// (config 4: 8192 x n=256, fp32 and fp64).
+//
+// Reference path per matrix: pfaffian -> ltlt_blk_piv(x, b=min(256, m))
+// (apps.py:12-30, blocked.py:303-363), i.e. one left-looking pivoted panel.
+// The B200 kernel factors each matrix with the right-looking Wimmer two-step
+// recurrence (unblocked.py:136-171) -- the same pivots and factors in exact
+// arithmetic -- inside ONE CTA: the trailing matrix lives in shared memory
+// (packed lower columns), the argmax is a warp redux over the column, the
+// symmetric interchange and the rank-2 update are CTA-parallel with only
+// __syncthreads between phases.  Columns that do not fit the shared-memory
+// budget (the first few columns in fp64) live in the output L buffer.
+// A persistent grid walks the batch; outputs: L ("ones" layout), tau,
+// relative pivots, and sign / log|Pf| (overflow-free apps.py:26-30).
+#include <cmath>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace skl {
+namespace {
+
+constexpr int kBThreads = 512;
+constexpr int kBWarps = kBThreads / 32;
+
+template <typename T>
+struct BCtx {
+  T* smem;    // packed columns j >= J0 (rows j+1..n-1)
+  T* gl;      // L buffer of this matrix (columns j < J0 live here)
+  long long ldl;
+  int n, J0;
+  __device__ __forceinline__ T* col(int j) const {
+    // pointer such that col(j)[i] is element (i, j), valid for i > j
+    if (j < J0) return gl + (long long)j * ldl;
+    // offset of column j in packed storage: sum_{c=J0}^{j-1} (n-1-c)
+    const long long off = (long long)(j - J0) * (n - 1) - ((long long)j * (j - 1) - (long long)J0 * (J0 - 1)) / 2;
+    return smem + off - (j + 1);
+  }
+};
+
+__device__ __forceinline__ int bwarp_argmax(double av, int idx, bool valid) {
+  const unsigned long long bits = valid ? (unsigned long long)__double_as_longlong(av) : 0ull;
+  const unsigned hi = valid ? unsigned(bits >> 32) + 1u : 0u;
+  const unsigned lo = unsigned(bits);
+  const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+  const bool c1 = valid && hi == m1;
+  const unsigned m2 = __reduce_max_sync(0xffffffffu, c1 ? lo : 0u);
+  const bool c2 = c1 && lo == m2;
+  const unsigned id = __reduce_min_sync(0xffffffffu, c2 ? unsigned(idx) : 0xffffffffu);
+  return id == 0xffffffffu ? -1 : int(id);
+}
+
+// iamax over X[g+1:, g] (ties -> lowest index); result broadcast through smem
+template <typename T>
+__device__ int col_argmax(const BCtx<T>& c, int g, int* red) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const T* x = c.col(g);
+  double bv = -1.0;
+  int bi = -1;
+  for (int i = g + 1 + tid; i < c.n; i += kBThreads) {
+    double v = fabs((double)x[i]);
+    if (v > bv) {
+      bv = v;
+      bi = i;
+    }
+  }
+  const int id = bwarp_argmax(bv, bi, bi >= 0);
+  if (lane == 0) red[warp] = id;
+  __syncthreads();
+  if (warp == 0) {
+    const int cand = lane < kBWarps ? red[lane] : -1;
+    const double v = cand >= 0 ? fabs((double)x[cand]) : 0.0;
+    const int id2 = bwarp_argmax(v, cand, cand >= 0);
+    if (lane == 0) red[kBWarps] = id2 < 0 ? g + 1 : id2;
+  }
+  __syncthreads();
+  return red[kBWarps];
+}
+
+// X := P X P^T for the transposition (a, b), a < b, over the whole matrix
+template <typename T>
+__device__ void bsym_swap(const BCtx<T>& c, int a, int b) {
+  const int tid = threadIdx.x, n = c.n;
+  // rows a, b of columns j < a
+  for (int j = tid; j < a; j += kBThreads) {
+    T* p = c.col(j);
+    T t = p[a];
+    p[a] = p[b];
+    p[b] = t;
+  }
+  T* pa = c.col(a);
+  T* pb = c.col(b);
+  // columns a, b below row b
+  for (int i = b + 1 + tid; i < n; i += kBThreads) {
+    T t = pa[i];
+    pa[i] = pb[i];
+    pb[i] = t;
+  }
+  // crossing (i, a) <-> -(b, i), a < i < b
+  for (int i = a + 1 + tid; i < b; i += kBThreads) {
+    T* pi = c.col(i);
+    T t = pi[b];
+    T u = pa[i];
+    pa[i] = -t;
+    pi[b] = -u;
+  }
+  if (tid == 0) pa[b] = -pa[b];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBThreads, 1)
+batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx, long long strideX, T* __restrict__ L,
+               long long ldl, long long strideL, T* __restrict__ tau, long long strideTau, long long* __restrict__ piv,
+               long long stridePiv, double* __restrict__ pf_sign, double* __restrict__ pf_logabs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* vec = reinterpret_cast<T*>(smem_raw);  // [2][n] rank-2 vectors
+  int* red = reinterpret_cast<int*>(vec + 2 * n);
+  T* store = reinterpret_cast<T*>(smem_raw + ((2 * n * sizeof(T) + (kBWarps + 2) * sizeof(int) + 15) & ~size_t(15)));
+  const int tid = threadIdx.x;
+
+  for (int m = blockIdx.x; m < batch; m += gridDim.x) {
+    const T* x = X + (long long)m * strideX;
+    T* l = L + (long long)m * strideL;
+    T* tm = tau + (long long)m * strideTau;
+    long long* pm = piv + (long long)m * stridePiv;
+    BCtx<T> c{store, l, ldl, n, J0};
+    // load (one flattened, coalesced pass): strictly-lower columns j >= J0 go
+    // to shared memory, everything else (upper/diag, columns j < J0) to L
+    {
+      const int nn = n * n;
+#pragma unroll 4
+      for (int e = tid; e < nn; e += kBThreads) {
+        const int j = e / n, i = e - j * n;
+        const T v = x[(long long)j * ldx + i];
+        if (i > j && j >= J0)
+          c.col(j)[i] = v;
+        else
+          l[(long long)j * ldl + i] = v;
+      }
+    }
+    if (tid == 0) pm[0] = 0;
+    __syncthreads();
+
+    int nswaps = 0;
+    double logabs = 0.0, sgn = 1.0;
+    const int end = n - 1;
+    int g = 0;
+    while (g < end) {
+      // ---- eliminate(g) ----------------------------------------------------
+      int b = col_argmax(c, g, red);
+      if (b != g + 1) bsym_swap(c, g + 1, b);
+      if (tid == 0) {
+        pm[g + 1] = b - (g + 1);
+        nswaps += b != g + 1;
+      }
+      __syncthreads();
+      T* xg = c.col(g);
+      const T t0 = xg[g + 1];
+      if (t0 != T(0))
+        for (int i = g + 2 + tid; i < n; i += kBThreads) xg[i] = xg[i] / t0;
+      if ((g & 1) == 0) {
+        // Pf = sign(P) prod_{i even} (-tau_i)
+        logabs += log(fabs((double)t0));
+        sgn *= (t0 > T(0)) ? -1.0 : (t0 < T(0) ? 1.0 : 0.0);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        tm[g] = t0;
+        xg[g + 1] = T(1);
+      }
+      if (g + 1 >= end) {
+        // odd leftover: rank-2 on [g+2:, g+2:] is empty when g + 2 == n
+        __syncthreads();
+        g += 1;
+        break;
+      }
+      // ---- eliminate(g+1) --------------------------------------------------
+      b = col_argmax(c, g + 1, red);
+      if (b != g + 2) bsym_swap(c, g + 2, b);
+      if (tid == 0) {
+        pm[g + 2] = b - (g + 2);
+        nswaps += b != g + 2;
+      }
+      __syncthreads();
+      // ---- tau[g+1], scale column g+1, fold into column g+2, rank-2 vectors --
+      const int s0 = g + 3;
+      T* x1 = c.col(g + 1);
+      T* x2 = c.col(g + 2);
+      const T t1 = x1[g + 2];
+      const T x20 = xg[g + 2];
+      for (int i = s0 + tid; i < n; i += kBThreads) {
+        const T l2 = t1 != T(0) ? x1[i] / t1 : x1[i];
+        x1[i] = l2;
+        const T l1i = xg[i];
+        const T f = x2[i] - t1 * (x20 * l2 - l1i);
+        x2[i] = f;
+        vec[i] = f - t1 * l1i;  // wv
+        vec[n + i] = l2;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        tm[g + 1] = t1;
+        x1[g + 2] = T(1);
+      }
+      // ---- X[s:, s:] -= wv l2^T - l2 wv^T -------------------------------------
+      if (s0 < n) {
+        // flattened strictly-lower trapezoid of the trailing block, column-major
+        // lane <-> rows i = s0 + lane + 32 r (wv_i, l2_i held in registers),
+        // warp <-> columns j = s0 + warp + kBWarps q (l2_j, wv_j broadcast)
+        const int lane = tid & 31, warp = tid >> 5;
+        if (n - s0 <= 256) {
+          T vi[8], ui[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int i = s0 + lane + 32 * r;
+            vi[r] = i < n ? vec[i] : T(0);
+            ui[r] = i < n ? vec[n + i] : T(0);
+          }
+          for (int j = s0 + warp; j < n - 1; j += kBWarps) {
+            T* p = c.col(j);
+            const T wj = vec[j], lj = vec[n + j];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const int i = s0 + lane + 32 * r;
+              if (i > j && i < n) p[i] -= vi[r] * lj - ui[r] * wj;
+            }
+          }
+        } else {
+          for (int j = s0 + warp; j < n - 1; j += kBWarps) {
+            T* p = c.col(j);
+            const T wj = vec[j], lj = vec[n + j];
+            for (int i = j + 1 + lane; i < n; i += 32) p[i] -= vec[i] * lj - vec[n + i] * wj;
+          }
+        }
+      }
+      __syncthreads();
+      g += 2;
+    }
+    if (tid == 0) {
+      if (n % 2 == 1) {
+        if (pf_sign) pf_sign[m] = 0.0;
+        if (pf_logabs) pf_logabs[m] = -INFINITY;
+      } else {
+        if (nswaps & 1) sgn = -sgn;
+        if (pf_sign) pf_sign[m] = sgn;
+        if (pf_logabs) pf_logabs[m] = sgn == 0.0 ? -INFINITY : logabs;
+      }
+    }
+    // write the packed columns back into L (flattened, coalesced)
+    {
+      const int nn = n * n;
+#pragma unroll 4
+      for (int e = tid; e < nn; e += kBThreads) {
+        const int j = e / n, i = e - j * n;
+        if (i > j && j >= J0) l[(long long)j * ldl + i] = c.col(j)[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+size_t batched_smem(int n, int J0) {
+  size_t head = (2 * n * sizeof(T) + (kBWarps + 2) * sizeof(int) + 15) & ~size_t(15);
+  long long cols = 0;
+  for (int j = J0; j < n - 1; ++j) cols += n - 1 - j;
+  return head + (size_t)cols * sizeof(T);
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_batched(int batch, int n, const T* X, long long ldx, long long strideX, T* L, long long ldl,
+                           long long strideL, T* tau, long long strideTau, long long* piv, long long stridePiv,
+                           double* pf_sign, double* pf_logabs, cudaStream_t stream) {
+  int dev = 0, lim = 0, nsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int J0 = 0;
+  while (J0 < n - 1 && batched_smem<T>(n, J0) > (size_t)lim) ++J0;
+  size_t smem = batched_smem<T>(n, J0);
+  cudaError_t e = cudaFuncSetAttribute(batched_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int grid = batch < nsm ? batch : nsm;
+  batched_kernel<T><<<grid, kBThreads, smem, stream>>>(batch, n, J0, X, ldx, strideX, L, ldl, strideL, tau, strideTau,
+                                                       piv, stridePiv, pf_sign, pf_logabs);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_batched<double>(int, int, const double*, long long, long long, double*, long long,
+                                            long long, double*, long long, long long*, long long, double*, double*,
+                                            cudaStream_t);
+template cudaError_t launch_batched<float>(int, int, const float*, long long, long long, float*, long long, long long,
+                                           float*, long long, long long*, long long, double*, double*, cudaStream_t);
+
+}  // namespace skl

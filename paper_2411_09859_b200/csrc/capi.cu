@@ -278,7 +278,7 @@ size_t skl_skr2k_workspace_size(int n, int k) {
   b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
   b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
   b.take<int>(std::max(k, 1));
-  b.take<int>(4);
+  b.take<int>(4 + std::max(k, 1));
   return b.off + 256;
 }
 
@@ -296,7 +296,7 @@ int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, 
   double* P = b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
   double* Q = b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
   int* keep = b.take<int>(std::max(k, 1));
-  int* cnt = b.take<int>(4);  // [0] keff, [1] nk4
+  int* cnt = b.take<int>(4 + std::max(k, 1));  // [0] keff, [1] nk4, [2..] per-column flags
   if (n <= 1 || k == 0 || alpha == 0.0) {
     if (n <= 1) {
       if (keff_dev) {

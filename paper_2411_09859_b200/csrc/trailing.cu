@@ -38,6 +38,11 @@ __device__ __forceinline__ size_t packed_off(int row, int col, int k4cap) {
   return (((size_t)t * k4cap + q) * 16 + mb) * 32 + (r8 * 4 + c4);
 }
 
+// Persistent lower-triangular DGEMM-NT: one CTA per SM walks the lower tiles
+// (ti >= tj) round-robin; the bulk-copy ring runs ahead across tile
+// boundaries so the next tile's operands stream in during the epilogue.  The
+// C tile is prefetched into L2 when a tile starts and read-modified-written
+// in the epilogue (accumulators start at zero).
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q, int k4cap, int nk4_host,
                      const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta) {
@@ -46,17 +51,39 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
   double* sQ = sP + kStages * kStageDoubles;
   uint64_t* full = reinterpret_cast<uint64_t*>(sQ + kStages * kStageDoubles);
 
-  // triangular tile index -> (ti, tj), ti >= tj
-  const int t = blockIdx.x;
-  int ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-  while (ti * (ti + 1) / 2 > t) --ti;
-  const int tj = t - ti * (ti + 1) / 2;
-
+  const int nt = tiles_for(n);
+  const int ntiles = nt * (nt + 1) / 2;
   const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
   const int nchunks = (nk4 + kK4PerStage - 1) / kK4PerStage;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 2, wn = warp & 3;
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int total_chunks = my_tiles * nchunks;
+  if (my_tiles == 0 || nchunks == 0) {
+    // nothing to multiply: still apply beta to the owned tiles
+    for (int t = blockIdx.x; t < ntiles && nchunks == 0; t += gridDim.x) {
+      int ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+      while (ti * (ti + 1) / 2 > t) --ti;
+      const int tj = t - ti * (ti + 1) / 2;
+      for (int e = tid; e < kTile * kTile; e += kGemmThreads) {
+        int row = ti * kTile + (e & (kTile - 1)), col = tj * kTile + (e >> 7);
+        if (row < n && col < n && row > col) {
+          double* p = C + (long long)col * ldc + row;
+          *p = beta == 0.0 ? 0.0 : beta * *p;
+        }
+      }
+    }
+    return;
+  }
+
+  auto tile_of = [&](int i, int& ti, int& tj) {
+    const int t = blockIdx.x + i * gridDim.x;
+    ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    while (ti * (ti + 1) / 2 > t) --ti;
+    tj = t - ti * (ti + 1) / 2;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
@@ -64,72 +91,95 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
   }
   __syncthreads();
 
-  const double* Pt = P + (size_t)ti * k4cap * kBlkDoubles;
-  const double* Qt = Q + (size_t)tj * k4cap * kBlkDoubles;
-  auto issue = [&](int chunk) {
-    int s = chunk % kStages;
-    int q0 = chunk * kK4PerStage;
-    int nb = min(kK4PerStage, nk4 - q0);
-    uint32_t bytes = uint32_t(nb) * kBlkDoubles * sizeof(double);
+  // global chunk q -> (tile i = q / nchunks, chunk c = q % nchunks)
+  auto issue = [&](int q) {
+    const int s = q % kStages;
+    const int i = q / nchunks, c = q - i * nchunks;
+    int ti, tj;
+    tile_of(i, ti, tj);
+    const int q0 = c * kK4PerStage;
+    const int nb = min(kK4PerStage, nk4 - q0);
+    const uint32_t bytes = uint32_t(nb) * kBlkDoubles * sizeof(double);
     mbar_arrive_expect_tx(&full[s], 2 * bytes);
-    bulk_g2s(sP + s * kStageDoubles, Pt + (size_t)q0 * kBlkDoubles, bytes, &full[s]);
-    bulk_g2s(sQ + s * kStageDoubles, Qt + (size_t)q0 * kBlkDoubles, bytes, &full[s]);
+    bulk_g2s(sP + s * kStageDoubles, P + ((size_t)ti * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
+    bulk_g2s(sQ + s * kStageDoubles, Q + ((size_t)tj * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
   };
   if (tid == 0) {
-    for (int c = 0; c < min(kStages, nchunks); ++c) issue(c);
+    for (int q = 0; q < min(kStages, total_chunks); ++q) issue(q);
   }
 
-  // accumulators initialised from beta*C (masked to the strictly-lower part)
-  double acc[8][4][2];
-  const int row_base = ti * kTile + wm * 64 + (lane >> 2);
-  const int col_base = tj * kTile + wn * 32 + 2 * (lane & 3);
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int row = row_base + mi * 8, col = col_base + ni * 8 + e;
-        double v = 0.0;
-        if (beta != 0.0 && row < n && col < n && row > col) v = beta * C[(long long)col * ldc + row];
-        acc[mi][ni][e] = v;
+  int q = 0;
+  for (int i = 0; i < my_tiles; ++i) {
+    int ti, tj;
+    tile_of(i, ti, tj);
+    // warm L2 with this tile's C columns (read-modify-written in the epilogue)
+    if (tid < kTile) {
+      const int col = tj * kTile + tid;
+      const int r0 = ti * kTile;
+      if (col < n && r0 < n) {
+        const int rows = min(kTile, n - r0);
+        const double* src = C + (long long)col * ldc + r0;
+        uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+        uintptr_t a1 = (reinterpret_cast<uintptr_t>(src + rows) + 15) & ~uintptr_t(15);
+        prefetch_l2_bulk(reinterpret_cast<const void*>(a0), uint32_t(a1 - a0));
       }
     }
-  }
+    double acc[8][4][2];
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
-  for (int c = 0; c < nchunks; ++c) {
-    const int s = c % kStages;
-    mbar_wait(&full[s], (c / kStages) & 1);
-    const int nb = min(kK4PerStage, nk4 - c * kK4PerStage);
-    const double* ps = sP + s * kStageDoubles + (wm * 8) * 32 + lane;
-    const double* qs = sQ + s * kStageDoubles + (wn * 4) * 32 + lane;
-    for (int kb = 0; kb < nb; ++kb) {
-      double a[8], b[4];
+    for (int c = 0; c < nchunks; ++c, ++q) {
+      const int s = q % kStages;
+      mbar_wait(&full[s], (q / kStages) & 1);
+      const int nb = min(kK4PerStage, nk4 - c * kK4PerStage);
+      const double* ps = sP + s * kStageDoubles + (wm * 8) * 32 + lane;
+      const double* qs = sQ + s * kStageDoubles + (wn * 4) * 32 + lane;
+      for (int kb = 0; kb < nb; ++kb) {
+        double a[8], b[4];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) a[mi] = ps[kb * kBlkDoubles + mi * 32];
+        for (int mi = 0; mi < 8; ++mi) a[mi] = ps[kb * kBlkDoubles + mi * 32];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = qs[kb * kBlkDoubles + ni * 32];
+        for (int ni = 0; ni < 4; ++ni) b[ni] = qs[kb * kBlkDoubles + ni * 32];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-    }
-    __syncthreads();  // every warp is done with stage s
-    if (tid == 0 && c + kStages < nchunks) {
-      fence_proxy_async();
-      issue(c + kStages);
-    }
-  }
-
-#pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int row = row_base + mi * 8, col = col_base + ni * 8 + e;
-        if (row < n && col < n && row > col) C[(long long)col * ldc + row] = acc[mi][ni][e];
+          for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
+      __syncthreads();  // every warp is done with stage s
+      if (tid == 0 && q + kStages < total_chunks) {
+        fence_proxy_async();
+        issue(q + kStages);
+      }
+    }
+
+    const int row_base = ti * kTile + wm * 64 + (lane >> 2);
+    const int col_base = tj * kTile + wn * 32 + 2 * (lane & 3);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // epilogue in two halves to bound register use
+      double cin[4][4][2];
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = row_base + (h * 4 + mm) * 8, col = col_base + ni * 8 + e;
+            cin[mm][ni][e] =
+                (beta != 0.0 && row < n && col < n && row > col) ? C[(long long)col * ldc + row] : 0.0;
+          }
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int row = row_base + (h * 4 + mm) * 8, col = col_base + ni * 8 + e;
+            if (row < n && col < n && row > col)
+              C[(long long)col * ldc + row] =
+                  (beta == 1.0 ? cin[mm][ni][e] : beta * cin[mm][ni][e]) + acc[h * 4 + mm][ni][e];
+          }
     }
   }
 }
@@ -184,15 +234,18 @@ __global__ void pack_rankk_kernel(const double* __restrict__ A, long long lda, i
 
 // keep[j] = column j is nonzero in both A and B (kernels3.py:318-321);
 // single CTA: flags, then an ordered compaction.
-__global__ void rank2k_keep_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B,
-                                   long long ldb, int n, int k, int skip_zero, int* __restrict__ keep,
-                                   int* __restrict__ keff_dev, int* __restrict__ nk4_dev) {
-  extern __shared__ int flags[];
-  for (int j = threadIdx.x >> 5; j < k; j += blockDim.x >> 5) {
+// grid (column groups, row chunks); flags[j] |= (chunk of A[:, j] nonzero) etc.
+// flags[j] bit 0: A column nonzero, bit 1: B column nonzero (zeroed by the launcher)
+__global__ void rank2k_flags_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B,
+                                    long long ldb, int n, int k, int skip_zero, int* __restrict__ flags) {
+  const int wpb = blockDim.x >> 5;
+  const int rchunk = (n + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * rchunk, r1 = min(n, r0 + rchunk);
+  for (int j = blockIdx.x * wpb + (threadIdx.x >> 5); j < k; j += gridDim.x * wpb) {
     int lane = threadIdx.x & 31;
     int nzA = 0, nzB = 0;
     if (skip_zero) {
-      for (int i = lane; i < n; i += 32) {
+      for (int i = r0 + lane; i < r1; i += 32) {
         nzA |= A[(long long)j * lda + i] != 0.0;
         nzB |= B[(long long)j * ldb + i] != 0.0;
       }
@@ -201,16 +254,33 @@ __global__ void rank2k_keep_kernel(const double* __restrict__ A, long long lda, 
     } else {
       nzA = nzB = 1;
     }
-    if (lane == 0) flags[j] = nzA && nzB;
+    if (lane == 0 && (nzA || nzB)) atomicOr(flags + j, (nzA ? 1 : 0) | (nzB ? 2 : 0));
   }
+}
+
+__global__ void rank2k_compact_kernel(const int* __restrict__ flags, int k, int* __restrict__ keep,
+                                      int* __restrict__ keff_dev, int* __restrict__ nk4_dev) {
+  __shared__ int cnt[1024];
+  const int per = (k + blockDim.x - 1) / blockDim.x;
+  const int j0 = threadIdx.x * per, j1 = min(k, j0 + per);
+  int c = 0;
+  for (int j = j0; j < j1; ++j) c += flags[j] == 3;
+  cnt[threadIdx.x] = c;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int c = 0;
-    for (int j = 0; j < k; ++j)
-      if (flags[j]) keep[c++] = j;
-    *keff_dev = c;
-    *nk4_dev = (2 * c + 3) / 4;
+    int acc = 0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      int v = cnt[t];
+      cnt[t] = acc;
+      acc += v;
+    }
+    *keff_dev = acc;
+    *nk4_dev = (2 * acc + 3) / 4;
   }
+  __syncthreads();
+  int o = cnt[threadIdx.x];
+  for (int j = j0; j < j1; ++j)
+    if (flags[j] == 3) keep[o++] = j;
 }
 
 // P = alpha*[A_keep | B_keep], Q = [B_keep | -A_keep]  => sum P Q^T = alpha (A B^T - B A^T)
@@ -250,8 +320,9 @@ __global__ void form_w_kernel(const double* __restrict__ A, long long lda, int n
     int j = int(e / n), i = int(e % n);
     double w = 0.0;
     if (j & 1) {
-      w = -tau[j - 1] * A[(long long)(j - 1) * lda + i];
-      if (j + 1 < k) w += tau[j] * A[(long long)(j + 1) * lda + i];
+      // two roundings, in the reference's entry order (no FMA contraction): bit-identical W
+      w = __dmul_rn(-tau[j - 1], A[(long long)(j - 1) * lda + i]);
+      if (j + 1 < k) w = __dadd_rn(w, __dmul_rn(tau[j], A[(long long)(j + 1) * lda + i]));
     }
     W[(long long)j * ldw + i] = w;
   }
@@ -275,9 +346,16 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
   int nt = tiles_for(n);
   int ntiles = nt * (nt + 1) / 2;
-  gemm_lower_nt_kernel<<<ntiles, kGemmThreads, kGemmSmem, stream>>>(P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta);
+  int grid = ntiles < nsm ? ntiles : nsm;
+  gemm_lower_nt_kernel<<<grid, kGemmThreads, kGemmSmem, stream>>>(P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta);
   return cudaGetLastError();
 }
 
@@ -291,8 +369,20 @@ cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, 
 
 cudaError_t launch_rank2k_keep(const double* A, long long lda, const double* B, long long ldb, int n, int k,
                                int skip_zero, int* keep, int* keff_dev, int* nk4_dev, cudaStream_t stream) {
-  rank2k_keep_kernel<<<1, 1024, sizeof(int) * (k > 0 ? k : 1), stream>>>(A, lda, B, ldb, n, k, skip_zero, keep,
-                                                                        keff_dev, nk4_dev);
+  // flags live in keep's tail half: keep has room for k entries, flags reuse nk4_dev+1.. is unsafe, so use
+  // the upper part of the keep array when k is small enough; the launcher passes a scratch via keff_dev+2
+  int* flags = keff_dev + 2;
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (k > 0 ? k : 1), stream);
+  if (e != cudaSuccess) return e;
+  int bx = (k + 7) / 8;
+  if (bx < 1) bx = 1;
+  int by = (n + 255) / 256;
+  if (by > 64) by = 64;
+  if (by < 1) by = 1;
+  rank2k_flags_kernel<<<dim3(bx, by), 256, 0, stream>>>(A, lda, B, ldb, n, k, skip_zero, flags);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  rank2k_compact_kernel<<<1, 1024, 0, stream>>>(flags, k, keep, keff_dev, nk4_dev);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,13 @@
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2411_09859_b200 import apps
+from paper_2411_09859_b200.inputs import skew_lower
+xs = np.stack([skew_lower(256, i) for i in range(8192)])
+for dt in (np.float64, np.float32):
+    xd = torch.from_numpy(np.ascontiguousarray(np.swapaxes(xs.astype(dt), 1, 2))).cuda()
+    for _ in range(2): apps.ltlt_batched_piv_device(xd)
+    torch.cuda.synchronize()
+    e0=torch.cuda.Event(enable_timing=True); e1=torch.cuda.Event(enable_timing=True)
+    e0.record(); apps.ltlt_batched_piv_device(xd); e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    print(dt.__name__, f"batched 8192x256: {ms:.2f} ms, {8192*256**3/3/ms/1e9:.2f} TFLOP/s", flush=True)
