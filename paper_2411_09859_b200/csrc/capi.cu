@@ -115,8 +115,14 @@ int env_int(const char* name, int dflt) {
 bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int rows = n - (lo + 1);
   static int no_cluster = env_int("SKL_NO_CLUSTER", 0);
-  const int C = no_cluster ? 0 : skl::panel_cluster_size();
-  if (C > 0) {
+  const int Cmax = no_cluster ? 0 : skl::panel_cluster_size();
+  if (Cmax > 0) {
+    // smallest cluster that keeps <= rows_target rows per CTA: fewer CTAs means a
+    // cheaper cluster barrier and less DSMEM fan-out of the pivot row per step
+    static int rows_target = env_int("SKL_CLUSTER_ROWS", 16);
+    int C = (rows + rows_target - 1) / rows_target;
+    if (C < 2) C = 2;
+    if (C > Cmax) C = Cmax;
     int Rc = (rows + C - 1) / C;
     if (Rc <= 1024) {
       int w = want;

@@ -92,6 +92,7 @@ struct CSmem {
   CCand* cand;     // [2][kClusterMax] written by every CTA of the cluster
   CCand* wcand;    // [kCWarps]
   int* misc;       // [0..1] pubA perm per parity, [2] local cand idx
+  int* pivbuf;     // [nelim] pivot offsets of this panel (flushed at the end)
 };
 
 __host__ __device__ inline int cslab_stride(int rows_per) { return rows_per | 1; }
@@ -134,6 +135,8 @@ __host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsign
   if (s) s->wcand = (CCand*)p;
   p = take(sizeof(int) * 8);
   if (s) s->misc = (int*)p;
+  p = take(sizeof(int) * (kmax + 2));
+  if (s) s->pivbuf = (int*)p;
   return off;
 }
 
@@ -231,6 +234,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 
   // per-thread rows: li = tid + u * kCThreads (R <= 2 * kCThreads)
   double cnext[2] = {0.0, 0.0};
+  bool cneg[2] = {false, false};  // gathered from the row part: negate at use (keeps the load in flight)
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int li = tid + u * kCThreads;
@@ -254,7 +258,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       const int li = tid + u * kCThreads;
       const int pos = rbase + li;
       if (li < rcount && pos > g) {
-        const double v = cnext[u] - s.az[li];
+        const double v = (cneg[u] ? -cnext[u] : cnext[u]) - s.az[li];
         col[li] = v;
         if (ibest < 0 || fabs(v) > fabs(vbest)) {
           vbest = v;
@@ -318,9 +322,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       const int li = tid + u * kCThreads;
       const int pos = rbase + li;
       cnext[u] = 0.0;
+      cneg[u] = false;
       if (more && li < rcount && pos > a_pos) {
         const int ph = (swapped && pos == b) ? perm_a : s.perm[li];
-        cnext[u] = skew_at(W, ld, ph, pb);
+        // X(ph, pb) in skew-lower storage; the sign is applied when consumed
+        cneg[u] = ph < pb;
+        cnext[u] = cneg[u] ? W[(long long)ph * ld + pb] : W[(long long)pb * ld + ph];
       }
     }
     {
@@ -368,10 +375,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       const double tj1 = (j + 1 == k) ? vb : s.taus[j + 1];
       s.zbuf[j] = (j >= 1 ? tj * xm : 0.0) - (j + 1 <= k ? tj1 * xp : 0.0);
     }
-    if (tid == 0 && cta == 0) {
-      a.tau[g] = vb;
-      a.piv[g + 1] = (long long)(b - a_pos);
-    }
+    if (tid == 0) s.pivbuf[g - r] = b - a_pos;  // tau is kept in s.taus
     __syncthreads();
     if (tid == 0) {
       s.taus[k] = vb;
@@ -401,6 +405,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     CMARK(4);
   }
   __syncthreads();
+  if (cta == 0) {
+    for (int g = r + tid; g < rt; g += kCThreads) {
+      a.tau[g] = s.taus[g - lo];
+      a.piv[g + 1] = (long long)s.pivbuf[g - r];
+    }
+  }
   if (a.prof && tid == 0) {
     for (int i = 0; i < 5; ++i) a.prof[cta * 8 + i] += (unsigned long long)pt[i];
     a.prof[cta * 8 + 5] += (unsigned long long)(rt - r);
@@ -409,7 +419,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int li = tid + u * kCThreads;
-      if (li < rcount) s.ycol[li] = cnext[u];
+      if (li < rcount) s.ycol[li] = cneg[u] ? -cnext[u] : cnext[u];
     }
   }
   __syncthreads();
