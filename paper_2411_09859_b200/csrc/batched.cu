@@ -25,16 +25,14 @@ constexpr int kBWarps = kBThreads / 32;
 
 template <typename T>
 struct BCtx {
-  T* smem;    // packed columns j >= J0 (rows j+1..n-1)
-  T* gl;      // L buffer of this matrix (columns j < J0 live here)
+  T* smem;           // packed columns j >= J0 (rows j+1..n-1)
+  T* gl;             // L buffer of this matrix (columns j < J0 live here)
+  const int* cofs;   // smem table: offset of column j in packed storage, minus (j+1)
   long long ldl;
   int n, J0;
   __device__ __forceinline__ T* col(int j) const {
     // pointer such that col(j)[i] is element (i, j), valid for i > j
-    if (j < J0) return gl + (long long)j * ldl;
-    // offset of column j in packed storage: sum_{c=J0}^{j-1} (n-1-c)
-    const long long off = (long long)(j - J0) * (n - 1) - ((long long)j * (j - 1) - (long long)J0 * (J0 - 1)) / 2;
-    return smem + off - (j + 1);
+    return j < J0 ? gl + (long long)j * ldl : smem + cofs[j];
   }
 };
 
@@ -115,15 +113,22 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* vec = reinterpret_cast<T*>(smem_raw);  // [2][n] rank-2 vectors
   int* red = reinterpret_cast<int*>(vec + 2 * n);
-  T* store = reinterpret_cast<T*>(smem_raw + ((2 * n * sizeof(T) + (kBWarps + 2) * sizeof(int) + 15) & ~size_t(15)));
+  int* cofs = red + kBWarps + 2;  // [n] column offsets
+  T* store = reinterpret_cast<T*>(smem_raw + ((2 * n * sizeof(T) + (kBWarps + 2 + n) * sizeof(int) + 15) & ~size_t(15)));
   const int tid = threadIdx.x;
+  for (int j = tid; j < n; j += kBThreads) {
+    // offset of column j >= J0: sum_{c=J0}^{j-1} (n-1-c), minus (j+1) so col(j)[i] indexes row i
+    const long long off = (long long)(j - J0) * (n - 1) - ((long long)j * (j - 1) - (long long)J0 * (J0 - 1)) / 2;
+    cofs[j] = j >= J0 ? int(off - (j + 1)) : 0;
+  }
+  __syncthreads();
 
   for (int m = blockIdx.x; m < batch; m += gridDim.x) {
     const T* x = X + (long long)m * strideX;
     T* l = L + (long long)m * strideL;
     T* tm = tau + (long long)m * strideTau;
     long long* pm = piv + (long long)m * stridePiv;
-    BCtx<T> c{store, l, ldl, n, J0};
+    BCtx<T> c{store, l, cofs, ldl, n, J0};
     // load (one flattened, coalesced pass): strictly-lower columns j >= J0 go
     // to shared memory, everything else (upper/diag, columns j < J0) to L
     {
@@ -158,7 +163,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
       const T t0 = xg[g + 1];
       if (t0 != T(0))
         for (int i = g + 2 + tid; i < n; i += kBThreads) xg[i] = xg[i] / t0;
-      if ((g & 1) == 0) {
+      if ((g & 1) == 0 && tid == 0) {
         // Pf = sign(P) prod_{i even} (-tau_i)
         logabs += log(fabs((double)t0));
         sgn *= (t0 > T(0)) ? -1.0 : (t0 < T(0) ? 1.0 : 0.0);
@@ -261,7 +266,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
 
 template <typename T>
 size_t batched_smem(int n, int J0) {
-  size_t head = (2 * n * sizeof(T) + (kBWarps + 2) * sizeof(int) + 15) & ~size_t(15);
+  size_t head = (2 * n * sizeof(T) + (kBWarps + 2 + n) * sizeof(int) + 15) & ~size_t(15);
   long long cols = 0;
   for (int j = J0; j < n - 1; ++j) cols += n - 1 - j;
   return head + (size_t)cols * sizeof(T);
