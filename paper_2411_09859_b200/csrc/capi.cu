@@ -114,6 +114,9 @@ int env_int(const char* name, int dflt) {
 
 bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int rows = n - (lo + 1);
+  // GPU panel width cap for the cluster panel (per-step cost grows with the width while the
+  // trailing DMMA GEMM is already efficient at K ~ 96); SKL_GPU_NB overrides.
+  static int gpu_nb = env_int("SKL_GPU_NB", 96);
   static int no_cluster = env_int("SKL_NO_CLUSTER", 0);
   const int Cmax = no_cluster ? 0 : skl::panel_cluster_size();
   if (Cmax > 0) {
@@ -125,7 +128,7 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
     if (C > Cmax) C = Cmax;
     int Rc = (rows + C - 1) / C;
     if (Rc <= 1024) {
-      int w = want;
+      int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
       while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo) > smem_limit()) --w;
       if (w >= 1 && w >= std::min(want, 64)) {
         p = PanelPlan{r, w, lo, C, Rc, r + w - lo, 1};

@@ -25,7 +25,8 @@ namespace cg = cooperative_groups;
 namespace skl {
 namespace {
 
-constexpr int kCThreads = 512;
+constexpr int kCThreads = 256;
+constexpr int kBank = 32;  // register-cached slab columns per bank (2 banks, rows li = tid only)
 constexpr int kCWarps = kCThreads / 32;
 constexpr int kClusterMax = 16;
 
@@ -232,6 +233,10 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     t_prev = _t;                    \
   } while (0)
 
+  // register cache of slab columns [0, kBank*nbank) for row li = tid (the gemv re-reads
+  // the slab every step; shared-memory bandwidth is its bound otherwise)
+  double rb[2][kBank];
+  int nbank = 0;
   // per-thread rows: li = tid + u * kCThreads (R <= 2 * kCThreads)
   double cnext[2] = {0.0, 0.0};
   bool cneg[2] = {false, false};  // gathered from the row part: negate at use (keeps the load in flight)
@@ -346,10 +351,26 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       if (own_a) {
         const int la = a_pos - rbase;
         for (int j = tid; j < k; j += kCThreads) s.slab[(size_t)j * Rs + la] = s.wrow[j];
+        if (tid == la && nbank > 0) {
+#pragma unroll
+          for (int q = 0; q < kBank; ++q) rb[0][q] = s.wrow[q];
+          if (nbank > 1) {
+#pragma unroll
+            for (int q = 0; q < kBank; ++q) rb[1][q] = s.wrow[kBank + q];
+          }
+        }
       }
       if (own_b) {
         const int lb = b - rbase;
         for (int j = tid; j < k; j += kCThreads) s.slab[(size_t)j * Rs + lb] = s.arow[j];
+        if (tid == lb && nbank > 0) {
+#pragma unroll
+          for (int q = 0; q < kBank; ++q) rb[0][q] = s.arow[q];
+          if (nbank > 1) {
+#pragma unroll
+            for (int q = 0; q < kBank; ++q) rb[1][q] = s.arow[kBank + q];
+          }
+        }
       }
     }
 #pragma unroll
@@ -381,16 +402,50 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       s.taus[k] = vb;
       s.wrow[k] = 1.0;
     }
+    CMARK(5);
 
     // ---- (5) A z for the next column, one thread per row (overlaps the gather) --
     if (more) {
       const int kk = k + 1;
+      // columns [kBank*m, kBank*(m+1)) are final once the next column is kk >= kBank*(m+1)
+      if (nbank < 2 && kk >= kBank * (nbank + 1) && tid < rcount) {
+        if (nbank == 0) {
+#pragma unroll
+          for (int q = 0; q < kBank; ++q) rb[0][q] = s.slab[(size_t)q * Rs + tid];
+        } else {
+#pragma unroll
+          for (int q = 0; q < kBank; ++q) rb[1][q] = s.slab[(size_t)(kBank + q) * Rs + tid];
+        }
+      }
+      if (nbank < 2 && kk >= kBank * (nbank + 1)) ++nbank;
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int li = tid + u * kCThreads;
         if (li < rcount && rbase + li > a_pos) {
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
           int j = 0;
+          if (u == 0 && nbank > 0) {
+            const double2* z2 = reinterpret_cast<const double2*>(s.zbuf);
+#pragma unroll
+            for (int q = 0; q < kBank; q += 4) {
+              const double2 za = z2[q >> 1], zb = z2[(q >> 1) + 1];
+              a0 = fma(rb[0][q], za.x, a0);
+              a1 = fma(rb[0][q + 1], za.y, a1);
+              a2 = fma(rb[0][q + 2], zb.x, a2);
+              a3 = fma(rb[0][q + 3], zb.y, a3);
+            }
+            if (nbank > 1) {
+#pragma unroll
+              for (int q = 0; q < kBank; q += 4) {
+                const double2 za = z2[(kBank + q) >> 1], zb = z2[((kBank + q) >> 1) + 1];
+                a0 = fma(rb[1][q], za.x, a0);
+                a1 = fma(rb[1][q + 1], za.y, a1);
+                a2 = fma(rb[1][q + 2], zb.x, a2);
+                a3 = fma(rb[1][q + 3], zb.y, a3);
+              }
+            }
+            j = kBank * nbank;
+          }
           for (; j + 3 < kk; j += 4) {
             a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
             a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
@@ -412,8 +467,8 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     }
   }
   if (a.prof && tid == 0) {
-    for (int i = 0; i < 5; ++i) a.prof[cta * 8 + i] += (unsigned long long)pt[i];
-    a.prof[cta * 8 + 5] += (unsigned long long)(rt - r);
+    for (int i = 0; i < 6; ++i) a.prof[cta * 8 + i] += (unsigned long long)pt[i];
+    a.prof[cta * 8 + 6] += (unsigned long long)(rt - r);
   }
   if (a.want_y) {
 #pragma unroll

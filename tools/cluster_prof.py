@@ -16,8 +16,8 @@ lib.skl_debug_set_panel_profile(buf.data_ptr())
 pk.ltlt_blk_piv_device(xd, b, "var1"); torch.cuda.synchronize()
 lib.skl_debug_set_panel_profile(None)
 p = buf.view(16, 8).cpu().numpy()
-names = ["argmax+publish", "pubrow copy", "cluster barrier", "winner+gather+rows", "swap/scale/z", "az+store"]
+names = ["v+warp_argmax", "cta_cand+publish", "cluster_barrier", "winner+gather+rowread", "gemv(az)", "swap/scale/z"]
 for c in (0, 7, 15):
-    steps = max(p[c, 5], 1)
-    tot = p[c, :5].sum()
-    print(f"cta {c}: {tot/steps:.0f} cyc/step over {steps} steps: " + ", ".join(f"{names[i]}={p[c,i]/steps:.0f}" for i in range(5)))
+    steps = max(p[c, 6], 1)
+    tot = p[c, :6].sum()
+    print(f"cta {c}: {tot/steps:.0f} cyc/step over {steps} steps: " + ", ".join(f"{names[i]}={p[c,i]/steps:.0f}" for i in range(6)))
