@@ -93,7 +93,8 @@ size_t mat_bytes(int rows, int cols, long long ld) {
 struct PanelPlan {
   int r, nelim, lo;
   int ctas, rows_per, kmax;
-  int cluster;  // 1: single-cluster DSMEM panel kernel, 0: grid-wide kernel
+  int cluster;  // 2: multi-cluster kernel, 1: single-cluster DSMEM panel kernel, 0: grid-wide kernel
+  int csize;    // cluster size (multi)
 };
 
 size_t smem_limit() {
@@ -131,7 +132,23 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
       while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo) > smem_limit()) --w;
       if (w >= 1 && w >= std::min(want, 64)) {
-        p = PanelPlan{r, w, lo, C, Rc, r + w - lo, 1};
+        p = PanelPlan{r, w, lo, C, Rc, r + w - lo, 1, C};
+        return true;
+      }
+    }
+  }
+  static int multi = env_int("SKL_MULTI_CLUSTER", 1);
+  if (Cmax > 0 && multi) {
+    for (int csize : {Cmax, 8}) {
+      const int Q = skl::panel_multi_clusters(csize, smem_limit());
+      if (Q < 2) continue;
+      const int P = Q * csize;
+      const int Rm = (rows + P - 1) / P;
+      if (Rm > 512) continue;
+      int w = want;
+      while (w >= 1 && skl::panel_cluster_smem_bytes(Rm, r + w - lo) > smem_limit()) --w;
+      if (w >= 1 && w >= std::min(want, 64)) {
+        p = PanelPlan{r, w, lo, P, Rm, r + w - lo, 2, csize};
         return true;
       }
     }
@@ -145,7 +162,7 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int nelim = want;
   while (nelim >= 1 && skl::panel_smem_bytes(R, r + nelim - lo) > smem_limit()) --nelim;
   if (nelim < 1) return false;
-  p = PanelPlan{r, nelim, lo, ctas, R, r + nelim - lo, 0};
+  p = PanelPlan{r, nelim, lo, ctas, R, r + nelim - lo, 0, 0};
   return true;
 }
 
@@ -195,6 +212,7 @@ struct BlkWorkspace {
   uint64_t* recs;
   double* crow;
   double* arowg;
+  double* pbuf;
   size_t ll_bytes;
   int k4cap, slot_words, np;
 };
@@ -213,6 +231,7 @@ size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base,
   int slot_words = 4 + 2 * (kmax + 2);
   BlkWorkspace w{};
   w.W = b.take<double>((size_t)n * n);
+  w.pbuf = b.take<double>((size_t)kmax * n);
   w.P = b.take<double>(skl::packed_elems(n, k4cap));
   w.Q = b.take<double>(skl::packed_elems(n, k4cap));
   w.side = b.take<double>((size_t)2 * (nelim_max + 1) * n);
@@ -479,6 +498,7 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     a.recs = ws.recs;
     a.crow = ws.crow;
     a.arowg = ws.arowg;
+    a.pbuf = ws.pbuf;
     a.tag0 = tag;
     a.nblocks = p.ctas;
     a.rows_per = p.rows_per;
@@ -489,7 +509,9 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     a.prof = g_prof;
     {
       KScope ks(KPANEL, st);
-      if (p.cluster)
+      if (p.cluster == 2)
+        SKL_TRY(skl::launch_panel_multi(a, p.csize, st));
+      else if (p.cluster == 1)
         SKL_TRY(skl::launch_panel_cluster(a, st));
       else
         SKL_TRY(skl::launch_panel(a, st));

@@ -68,6 +68,7 @@ struct PanelArgs {
   uint64_t* recs;        // LL candidate records [2][P][4]
   double* crow;          // cluster panel: candidate rows [2][C][kmax+2]
   double* arowg;         // cluster panel: row a [2][kmax+2]
+  double* pbuf;          // multi-cluster panel: slab output [kmax][n]
   uint32_t tag0;         // first LL tag of this panel
   int nblocks;           // CTAs (co-resident)
   int rows_per;          // rows per CTA
@@ -84,6 +85,9 @@ cudaError_t launch_panel(const PanelArgs& a, cudaStream_t stream);
 int panel_cluster_size();
 size_t panel_cluster_smem_bytes(int rows_per, int kmax);
 cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
+// multi-cluster variant (cooperative; intra-cluster DSMEM + inter-cluster LL exchange)
+int panel_multi_clusters(int csize, size_t smem);
+cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream);
 
 cudaError_t launch_compose_suffix(const int* gperm_all, int npanels, const int* row0s, int n, int* sigma_all,
                                   cudaStream_t stream);

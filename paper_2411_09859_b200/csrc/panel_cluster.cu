@@ -92,8 +92,9 @@ struct CSmem {
   int* perm;       // [Rs]
   CCand* cand;     // [2][kClusterMax] written by every CTA of the cluster
   CCand* wcand;    // [kCWarps]
-  int* misc;       // [0..1] pubA perm per parity, [2] local cand idx
+  int* misc;       // [0..1] pubA perm per parity, [4..5] global winner owner (MULTI)
   int* pivbuf;     // [nelim] pivot offsets of this panel (flushed at the end)
+  CCand* gwin;     // [2] global winner (MULTI)
 };
 
 __host__ __device__ inline int cslab_stride(int rows_per) { return rows_per | 1; }
@@ -138,6 +139,8 @@ __host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsign
   if (s) s->misc = (int*)p;
   p = take(sizeof(int) * (kmax + 2));
   if (s) s->pivbuf = (int*)p;
+  p = take(sizeof(CCand) * 2);
+  if (s) s->gwin = (CCand*)p;
   return off;
 }
 
@@ -186,10 +189,19 @@ __device__ __forceinline__ void compute_az(const CSmem& s, int Rs, int R, int rc
   }
 }
 
+// MULTI = several co-resident clusters (cooperative launch): candidates are
+// reduced inside each cluster through DSMEM, then the cluster leaders exchange
+// their cluster's best through global LL records; pivot rows travel through L2.
+template <bool MULTI>
 __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cg::cluster_group cluster = cg::this_cluster();
-  const int C = gridDim.x, cta = blockIdx.x;
+  const int C = MULTI ? int(cluster.num_blocks()) : int(gridDim.x);
+  const int crank = MULTI ? int(cluster.block_rank()) : int(blockIdx.x);  // rank inside the cluster
+  const int gcta = blockIdx.x;                                             // global CTA id (row owner)
+  const int Q = MULTI ? int(gridDim.x) / C : 1;                            // clusters
+  const int qid = gcta / C;
+  const int cta = gcta;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n, lo = a.lo, r = a.r, nelim = a.nelim, kmax = a.kmax;
   const int R = a.rows_per, Rs = cslab_stride(R);
@@ -252,8 +264,9 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     const int par = g & 1;
     double* col = s.slab + (size_t)k * Rs;
     const int a_pos = g + 1;
-    const int owner_a = (a_pos - row0) / R;
+    const int owner_a = (a_pos - row0) / R;  // global CTA id owning position a
     const bool own_a = owner_a == cta;
+    const uint32_t tag = a.tag0 + uint32_t(g - r);
 
     // ---- (1) v = c - A z; per-warp argmax -----------------------------------
     double vbest = 0.0;
@@ -291,15 +304,26 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         c.perm = s.perm[c.idx - rbase];
         const int lc = c.idx - rbase;
         double* pr = s.pubrow + par * (kmax + 2);
-        for (int j = lane; j <= k; j += 32) pr[j] = s.slab[(size_t)j * Rs + lc];
+        if (MULTI) {
+          uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
+          for (int j = lane; j <= k; j += 32) ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc], tag);
+        } else {
+          for (int j = lane; j <= k; j += 32) pr[j] = s.slab[(size_t)j * Rs + lc];
+        }
       }
       __syncwarp();
-      if (lane < C) *cluster.map_shared_rank(s.cand + par * kClusterMax + cta, lane) = c;
+      if (lane < C) *cluster.map_shared_rank(s.cand + par * kClusterMax + crank, lane) = c;
     } else if (warp == 1 && own_a) {
       const int la = a_pos - rbase;
-      double* pa = s.pubA + par * (kmax + 2);
-      for (int j = lane; j <= k; j += 32) pa[j] = s.slab[(size_t)j * Rs + la];
-      if (lane == 0) s.misc[par] = s.perm[la];
+      if (MULTI) {
+        uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
+        for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
+        if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
+      } else {
+        double* pa = s.pubA + par * (kmax + 2);
+        for (int j = lane; j <= k; j += 32) pa[j] = s.slab[(size_t)j * Rs + la];
+        if (lane == 0) s.misc[par] = s.perm[la];
+      }
     }
     CMARK(1);
     cluster_barrier();
@@ -314,6 +338,47 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       const int id = warp_argmax_redux(mine.v, mine.idx, ok);
       owner = __ffs(__ballot_sync(0xffffffffu, ok && mine.idx == id)) - 1;
       w = s.cand[par * kClusterMax + owner];
+      owner += qid * C;  // global CTA id of the cluster's best
+    }
+    if (MULTI) {
+      if (crank == 0 && warp == 0) {
+        // leader: publish the cluster's best, gather every cluster's best (one lane each)
+        uint64_t* rec = a.recs + ((size_t)par * Q + qid) * 6;
+        if (lane == 0) {
+          const uint64_t bits = __double_as_longlong(w.v);
+          ll_put2(rec, uint32_t(bits), uint32_t(bits >> 32), tag);
+          ll_put2(rec + 2, uint32_t(w.idx), uint32_t(w.perm), tag);
+          ll_put2(rec + 4, uint32_t(owner), 0u, tag);
+        }
+        CCand o{0.0, -1, -1};
+        int oo = -1;
+        if (lane < Q) {
+          const uint64_t* rq = a.recs + ((size_t)par * Q + lane) * 6;
+          uint32_t lo32, hi32, ci, cp, ow, dummy;
+          ll_get2(rq, tag, lo32, hi32);
+          ll_get2(rq + 2, tag, ci, cp);
+          ll_get2(rq + 4, tag, ow, dummy);
+          o.v = __longlong_as_double((long long)((uint64_t(hi32) << 32) | lo32));
+          o.idx = int(ci);
+          o.perm = int(cp);
+          oo = int(ow);
+        }
+        const bool ok = lane < Q && o.idx >= 0;
+        const int id = warp_argmax_redux(o.v, o.idx, ok);
+        const int wl = __ffs(__ballot_sync(0xffffffffu, ok && o.idx == id)) - 1;
+        CCand gw;
+        gw.v = __shfl_sync(0xffffffffu, o.v, wl);
+        gw.idx = __shfl_sync(0xffffffffu, o.idx, wl);
+        gw.perm = __shfl_sync(0xffffffffu, o.perm, wl);
+        const int gow = __shfl_sync(0xffffffffu, oo, wl);
+        if (lane < C) {
+          *cluster.map_shared_rank(s.gwin + par, lane) = gw;
+          *cluster.map_shared_rank(s.misc + 4 + par, lane) = gow;
+        }
+      }
+      cluster_barrier();
+      w = s.gwin[par];
+      owner = s.misc[4 + par];
     }
     const int b = w.idx, pb = w.perm;
     const double vb = w.v;
@@ -321,7 +386,15 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     const bool swapped = b != a_pos;
     const bool more = (g + 1 < rt) || a.want_y;
     int perm_a = 0;
-    if (own_b && swapped) perm_a = *cluster.map_shared_rank(s.misc + par, owner_a);
+    if (own_b && swapped) {
+      if (MULTI) {
+        uint32_t pa32, dummy;
+        ll_get2(a.rowa + (size_t)par * a.slot_words, tag, pa32, dummy);
+        perm_a = int(pa32);
+      } else {
+        perm_a = *cluster.map_shared_rank(s.misc + par, owner_a);
+      }
+    }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int li = tid + u * kCThreads;
@@ -335,7 +408,14 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         cnext[u] = cneg[u] ? W[(long long)ph * ld + pb] : W[(long long)pb * ld + ph];
       }
     }
-    {
+    if (MULTI) {
+      const uint64_t* gr = a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4;
+      for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = ll_get_double(gr + 2 * j, tag);
+      if (own_b && swapped) {
+        const uint64_t* ra = a.rowa + (size_t)par * a.slot_words + 4;
+        for (int j = tid; j <= k; j += kCThreads) s.arow[j] = ll_get_double(ra + 2 * j, tag);
+      }
+    } else {
       const double* wr = cluster.map_shared_rank(s.pubrow + par * (kmax + 2), owner);
       for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = wr[j];
       if (own_b && swapped) {
@@ -497,6 +577,15 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   if (cta == 0) {
     for (int i = tid; i < row0; i += kCThreads) a.gperm[i] = i;
   }
+  if (MULTI) {
+    // the slab goes to the panel buffer; panel_finish_* (separate launches, a grid-wide
+    // ordering point) materialise the displaced lines and write the L columns
+    for (int j = 0; j < kmax; ++j) {
+      const double* sc = s.slab + (size_t)j * Rs;
+      for (int li = tid; li < rcount; li += kCThreads) a.pbuf[(size_t)j * n + rbase + li] = sc[li];
+    }
+    return;
+  }
   __threadfence();
   cluster_barrier();
   const int nd = *((volatile int*)a.disp_count);
@@ -530,6 +619,43 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   }
 }
 
+// MULTI panel epilogue, launch 1: displaced trailing lines -> side buffer (reads W only)
+__global__ void panel_finish_gather(PanelArgs a) {
+  const int n = a.n, rt = a.r + a.nelim, ntr = n - rt;
+  const int nd = *a.disp_count;
+  for (int q = blockIdx.y; q < nd; q += gridDim.y) {
+    const int p = a.disp_list[q];
+    const int pp = a.gperm[p];
+    double* line = a.side + (size_t)q * ntr;
+    for (int i = rt + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+      line[i - rt] = (i == p) ? 0.0 : skew_at(a.W, a.ld, a.gperm[i], pp);
+  }
+}
+
+// MULTI panel epilogue, launch 2: panel buffer -> L columns [lo, rt); side -> trailing lines
+__global__ void panel_finish_write(PanelArgs a) {
+  const int n = a.n, lo = a.lo, rt = a.r + a.nelim, ntr = n - rt, row0 = lo + 1;
+  const long long ld = a.ld;
+  for (int j = blockIdx.y; j < a.kmax; j += gridDim.y) {
+    const int c = lo + j;
+    for (int pos = max(row0, c + 1) + blockIdx.x * blockDim.x + threadIdx.x; pos < n; pos += gridDim.x * blockDim.x)
+      a.W[(long long)c * ld + pos] = a.pbuf[(size_t)j * n + pos];
+  }
+  const int nd = *a.disp_count;
+  for (int q = blockIdx.y; q < nd; q += gridDim.y) {
+    const int p = a.disp_list[q];
+    const double* line = a.side + (size_t)q * ntr;
+    for (int i = rt + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const double v = line[i - rt];
+      if (i > p)
+        a.W[(long long)p * ld + i] = v;
+      else if (i < p)
+        a.W[(long long)i * ld + p] = -v;
+    }
+  }
+}
+
+
 }  // namespace
 
 size_t panel_cluster_smem_bytes(int rows_per, int kmax) { return csmem_layout(rows_per, kmax, nullptr, nullptr); }
@@ -539,8 +665,8 @@ int panel_cluster_size() {
   if (cs < 0) {
     cs = 0;
     for (int c : {16, 8}) {
-      cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(panel_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(panel_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c);
       cfg.blockDim = dim3(kCThreads);
@@ -553,7 +679,7 @@ int panel_cluster_size() {
       cfg.attrs = &attr;
       cfg.numAttrs = 1;
       int ncl = 0;
-      if (cudaOccupancyMaxActiveClusters(&ncl, panel_cluster_kernel, &cfg) == cudaSuccess && ncl >= 1) {
+      if (cudaOccupancyMaxActiveClusters(&ncl, panel_cluster_kernel<false>, &cfg) == cudaSuccess && ncl >= 1) {
         cs = c;
         break;
       }
@@ -566,9 +692,9 @@ int panel_cluster_size() {
 cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream) {
   const int C = a.nblocks;
   size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr);
-  cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = cudaFuncSetAttribute(panel_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
@@ -584,7 +710,69 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream) {
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, panel_cluster_kernel, a);
+  return cudaLaunchKernelEx(&cfg, panel_cluster_kernel<false>, a);
+}
+
+// Largest number of co-resident clusters of size `csize` for a given smem size (0: none).
+int panel_multi_clusters(int csize, size_t smem) {
+  cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = dim3(kCThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = csize;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, panel_cluster_kernel<true>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return ncl > 32 ? 32 : ncl;
+}
+
+// a.nblocks = total CTAs (Q clusters x a.csize); cooperative so all clusters are co-resident
+cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream) {
+  size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr);
+  cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.nblocks);
+  cfg.blockDim = dim3(kCThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = csize;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeCooperative;
+  attrs[1].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel<true>, a);
+  if (e != cudaSuccess) return e;
+  const int ntr = a.n - (a.r + a.nelim);
+  dim3 grid(ntr > 0 ? (ntr + 255) / 256 : 1, 2 * (a.nelim + 1));
+  if (grid.x > 16) grid.x = 16;
+  panel_finish_gather<<<grid, 256, 0, stream>>>(a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  dim3 grid2(grid.x, a.kmax > 2 * (a.nelim + 1) ? a.kmax : 2 * (a.nelim + 1));
+  panel_finish_write<<<grid2, 256, 0, stream>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace skl

@@ -8,16 +8,17 @@ from paper_2411_09859_b200.inputs import skew_lower
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 b = int(sys.argv[2]) if len(sys.argv) > 2 else 128
 xd = dv.to_device_colmajor(skew_lower(n, 0))
+import os
 lib = _capi.load()
 pk.ltlt_blk_piv_device(xd, b, "var1"); torch.cuda.synchronize()
-buf = torch.zeros(16 * 8, dtype=torch.int64, device="cuda")
+buf = torch.zeros(160 * 8, dtype=torch.int64, device="cuda")
 lib.skl_debug_set_panel_profile.argtypes = [ctypes.c_void_p]
 lib.skl_debug_set_panel_profile(buf.data_ptr())
 pk.ltlt_blk_piv_device(xd, b, "var1"); torch.cuda.synchronize()
 lib.skl_debug_set_panel_profile(None)
-p = buf.view(16, 8).cpu().numpy()
+p = buf.view(160, 8).cpu().numpy()
 names = ["v+warp_argmax", "cta_cand+publish", "cluster_barrier", "winner+gather+rowread", "gemv(az)", "swap/scale/z"]
-for c in (0, 7, 15):
+for c in ([0, 7, 15] if n <= 8192 else [0, 8, 63, 127]):
     steps = max(p[c, 6], 1)
     tot = p[c, :6].sum()
     print(f"cta {c}: {tot/steps:.0f} cyc/step over {steps} steps: " + ", ".join(f"{names[i]}={p[c,i]/steps:.0f}" for i in range(6)))
