@@ -142,6 +142,57 @@ def fp64_gemm_peak(torch):
     return 2 * n ** 3 / (best * 1e-3) / 1e12
 
 
+def _time(torch, fn, reps, e0, e1, flush=None):
+    out = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        torch.cuda.synchronize()
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return statistics.median(out)
+
+
+def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush):
+    """Configs 1, 3, 4 of BASELINE.json on this GPU (device-resident inputs)."""
+    from paper_2411_09859_b200 import apps
+    from paper_2411_09859_b200.inputs import skew_lower
+    from paper_2411_09859_b200.unblocked import ltlt_unb_twostep_device
+    res = {}
+    # config 1: unblocked Wimmer two-step, pivoted, n=512
+    x1 = dv.to_device_colmajor(skew_lower(512, 0))
+    for _ in range(3):
+        ltlt_unb_twostep_device(x1, True)
+    ms = _time(torch, lambda: ltlt_unb_twostep_device(x1, True), 10, e0, e1)
+    res["config1_twostep_n512"] = {"ms": round(ms, 4), "gflops": round(512 ** 3 / 3 / (ms * 1e-3) / 1e9, 2)}
+    # config 3: blocked n=16384, nb=256, U(-1,1)
+    x3 = dv.to_device_colmajor(skew_lower(16384, 0, "uniform"))
+    L3 = dv.empty_colmajor(16384, 16384, torch.float64)
+    t3 = torch.empty(16383, dtype=torch.float64, device="cuda")
+    p3 = torch.empty(16384, dtype=torch.int64, device="cuda")
+    pk.ltlt_blk_piv_device(x3, 256, "var1", out=(L3, t3, p3))
+    ms = _time(torch, lambda: pk.ltlt_blk_piv_device(x3, 256, "var1", out=(L3, t3, p3)), 2, e0, e1, flush)
+    g3 = 16384 ** 3 / 3 / (ms * 1e-3) / 1e9
+    res["config3_blk_piv_n16384_nb256"] = {"ms": round(ms, 2), "gflops": round(g3, 1),
+                                           "pct_fp64_peak": round(100 * g3 / 1e3 / fp64_peak, 2)}
+    del x3, L3
+    torch.cuda.empty_cache()
+    # config 4: 8192 independent n=256 factorizations + Pfaffians, fp64 and fp32
+    xs = np.stack([skew_lower(256, i) for i in range(8192)])
+    for name, dt in (("f64", np.float64), ("f32", np.float32)):
+        xd = torch.from_numpy(np.ascontiguousarray(np.swapaxes(xs.astype(dt), 1, 2))).cuda()
+        apps.ltlt_batched_piv_device(xd)
+        ms = _time(torch, lambda: apps.ltlt_batched_piv_device(xd), 3, e0, e1, flush)
+        res[f"config4_batched_8192x256_{name}"] = {"ms": round(ms, 3),
+                                                   "gflops": round(8192 * 256 ** 3 / 3 / (ms * 1e-3) / 1e9, 1),
+                                                   "pfaffians_per_s": round(8192 / (ms * 1e-3), 0)}
+        del xd
+    return res
+
+
 def cpu_baseline_port(x, budget_s=30.0):
     """The oracle (NumPy restatement of the reference) on the host cores."""
     import oracle
@@ -197,6 +248,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-other", action="store_true", help="skip the secondary config 1/3/4 measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args.gpus)
@@ -332,6 +384,11 @@ def main():
             skr_ms.append(e0.elapsed_time(e1))
     skr = SKR2K_FLOPS / (statistics.median(skr_ms) * 1e-3) / 1e9
 
+    # ---- the other BASELINE configs (secondary; not the headline value) ---------------
+    other = {}
+    if not args.skip_other and world == 1:
+        other = other_configs(torch, pk, dv, fp64_peak, e0, e1, flush)
+
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
@@ -351,6 +408,7 @@ def main():
                 "d2h_bytes_per_step": N * N * 8 + (N - 1) * 8 + N * 8, "ms_per_step": round(e2e, 4)},
         "gpu_launches": launches,
         "clocks": clocks,
+        "other_configs": other,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         val, reps, dt = cpu_baseline_port(x)
