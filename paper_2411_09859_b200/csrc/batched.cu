@@ -22,6 +22,7 @@ namespace {
 
 constexpr int kBThreads = 512;
 constexpr int kBWarps = kBThreads / 32;
+constexpr size_t kRedBytes = 2 * kBWarps * (sizeof(double) + sizeof(int));
 
 template <typename T>
 struct BCtx {
@@ -48,9 +49,11 @@ __device__ __forceinline__ int bwarp_argmax(double av, int idx, bool valid) {
   return id == 0xffffffffu ? -1 : int(id);
 }
 
-// iamax over X[g+1:, g] (ties -> lowest index); result broadcast through smem
+// iamax over X[g+1:, g] (ties -> lowest index).  One barrier: per-warp
+// partials in smem, then every warp reduces the partials redundantly.
+// `red` holds [2][kBWarps] (double-buffered by column parity).
 template <typename T>
-__device__ int col_argmax(const BCtx<T>& c, int g, int* red) {
+__device__ int col_argmax(const BCtx<T>& c, int g, double* redv, int* redi) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const T* x = c.col(g);
   double bv = -1.0;
@@ -63,16 +66,59 @@ __device__ int col_argmax(const BCtx<T>& c, int g, int* red) {
     }
   }
   const int id = bwarp_argmax(bv, bi, bi >= 0);
-  if (lane == 0) red[warp] = id;
-  __syncthreads();
-  if (warp == 0) {
-    const int cand = lane < kBWarps ? red[lane] : -1;
-    const double v = cand >= 0 ? fabs((double)x[cand]) : 0.0;
-    const int id2 = bwarp_argmax(v, cand, cand >= 0);
-    if (lane == 0) red[kBWarps] = id2 < 0 ? g + 1 : id2;
+  const int slot = (g & 1) * kBWarps;
+  if (bi >= 0 && bi == id) {
+    redv[slot + warp] = bv;
+    redi[slot + warp] = bi;
   }
+  if (lane == 0 && id < 0) redi[slot + warp] = -1;
   __syncthreads();
-  return red[kBWarps];
+  const int cand = lane < kBWarps ? redi[slot + lane] : -1;
+  const double v = cand >= 0 ? redv[slot + lane] : 0.0;
+  const int id2 = bwarp_argmax(v, cand, cand >= 0);
+  return id2 < 0 ? g + 1 : id2;
+}
+
+// Interchange (a = g+1, b) over the whole matrix fused with the elimination
+// of column g: L[:, g] = X[:, g] / tau below the unit (tau = X[b, g] before the
+// interchange), explicit 1 at [a, g].  Element sets are disjoint, so one pass.
+template <typename T>
+__device__ void swap_and_eliminate(const BCtx<T>& c, int g, int b, T tau) {
+  const int tid = threadIdx.x, n = c.n;
+  const int a = g + 1;
+  const bool sw = b != a;
+  // column g: finalize
+  T* xg = c.col(g);
+  {
+    const T vb_old_a = xg[a];  // value that moves to row b
+    for (int i = a + 1 + tid; i < n; i += kBThreads) {
+      T v = (sw && i == b) ? vb_old_a : xg[i];
+      xg[i] = tau != T(0) ? v / tau : v;
+    }
+  }
+  if (!sw) return;
+  // rows a, b of the older columns j < g
+  for (int j = tid; j < g; j += kBThreads) {
+    T* p = c.col(j);
+    T t = p[a];
+    p[a] = p[b];
+    p[b] = t;
+  }
+  T* pa = c.col(a);
+  T* pb = c.col(b);
+  for (int i = b + 1 + tid; i < n; i += kBThreads) {
+    T t = pa[i];
+    pa[i] = pb[i];
+    pb[i] = t;
+  }
+  for (int i = a + 1 + tid; i < b; i += kBThreads) {
+    T* pi = c.col(i);
+    T t = pi[b];
+    T u = pa[i];
+    pa[i] = -t;
+    pi[b] = -u;
+  }
+  if (tid == 0) pa[b] = -pa[b];
 }
 
 // X := P X P^T for the transposition (a, b), a < b, over the whole matrix
@@ -111,10 +157,11 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
                long long ldl, long long strideL, T* __restrict__ tau, long long strideTau, long long* __restrict__ piv,
                long long stridePiv, double* __restrict__ pf_sign, double* __restrict__ pf_logabs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* vec = reinterpret_cast<T*>(smem_raw);  // [2][n] rank-2 vectors
-  int* red = reinterpret_cast<int*>(vec + 2 * n);
-  int* cofs = red + kBWarps + 2;  // [n] column offsets
-  T* store = reinterpret_cast<T*>(smem_raw + ((2 * n * sizeof(T) + (kBWarps + 2 + n) * sizeof(int) + 15) & ~size_t(15)));
+  double* redv = reinterpret_cast<double*>(smem_raw);  // [2][kBWarps] argmax partials
+  int* redi = reinterpret_cast<int*>(redv + 2 * kBWarps);
+  T* vec = reinterpret_cast<T*>(smem_raw + kRedBytes);  // [2][n] rank-2 vectors
+  int* cofs = reinterpret_cast<int*>(vec + 2 * n);      // [n] column offsets
+  T* store = reinterpret_cast<T*>(smem_raw + ((kRedBytes + 2 * n * sizeof(T) + n * sizeof(int) + 15) & ~size_t(15)));
   const int tid = threadIdx.x;
   for (int j = tid; j < n; j += kBThreads) {
     // offset of column j >= J0: sum_{c=J0}^{j-1} (n-1-c), minus (j+1) so col(j)[i] indexes row i
@@ -151,51 +198,46 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
     const int end = n - 1;
     int g = 0;
     while (g < end) {
-      // ---- eliminate(g) ----------------------------------------------------
-      int b = col_argmax(c, g, red);
-      if (b != g + 1) bsym_swap(c, g + 1, b);
+      // ---- eliminate(g): argmax, interchange + scale in one pass -------------
+      int b = col_argmax(c, g, redv, redi);
+      const T t0 = c.col(g)[b];  // becomes X[g+1, g] after the interchange
+      __syncthreads();            // every warp has read the partials and tau
+      swap_and_eliminate(c, g, b, t0);
       if (tid == 0) {
         pm[g + 1] = b - (g + 1);
         nswaps += b != g + 1;
-      }
-      __syncthreads();
-      T* xg = c.col(g);
-      const T t0 = xg[g + 1];
-      if (t0 != T(0))
-        for (int i = g + 2 + tid; i < n; i += kBThreads) xg[i] = xg[i] / t0;
-      if ((g & 1) == 0 && tid == 0) {
-        // Pf = sign(P) prod_{i even} (-tau_i)
-        logabs += log(fabs((double)t0));
-        sgn *= (t0 > T(0)) ? -1.0 : (t0 < T(0) ? 1.0 : 0.0);
-      }
-      __syncthreads();
-      if (tid == 0) {
         tm[g] = t0;
-        xg[g + 1] = T(1);
+        if ((g & 1) == 0) {  // Pf = sign(P) prod_{i even} (-tau_i)
+          logabs += log(fabs((double)t0));
+          sgn *= (t0 > T(0)) ? -1.0 : (t0 < T(0) ? 1.0 : 0.0);
+        }
       }
+      __syncthreads();
+      if (tid == 0) c.col(g)[g + 1] = T(1);
       if (g + 1 >= end) {
-        // odd leftover: rank-2 on [g+2:, g+2:] is empty when g + 2 == n
         __syncthreads();
         g += 1;
         break;
       }
-      // ---- eliminate(g+1) --------------------------------------------------
-      b = col_argmax(c, g + 1, red);
-      if (b != g + 2) bsym_swap(c, g + 2, b);
+      // ---- eliminate(g+1) -----------------------------------------------------
+      b = col_argmax(c, g + 1, redv, redi);
+      const T t1 = c.col(g + 1)[b];
+      __syncthreads();
+      swap_and_eliminate(c, g + 1, b, t1);
       if (tid == 0) {
         pm[g + 2] = b - (g + 2);
         nswaps += b != g + 2;
+        tm[g + 1] = t1;
       }
       __syncthreads();
-      // ---- tau[g+1], scale column g+1, fold into column g+2, rank-2 vectors --
+      // ---- fold the first coupling into column g+2, rank-2 vectors ----------
       const int s0 = g + 3;
+      T* xg = c.col(g);
       T* x1 = c.col(g + 1);
       T* x2 = c.col(g + 2);
-      const T t1 = x1[g + 2];
       const T x20 = xg[g + 2];
       for (int i = s0 + tid; i < n; i += kBThreads) {
-        const T l2 = t1 != T(0) ? x1[i] / t1 : x1[i];
-        x1[i] = l2;
+        const T l2 = x1[i];
         const T l1i = xg[i];
         const T f = x2[i] - t1 * (x20 * l2 - l1i);
         x2[i] = f;
@@ -203,10 +245,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         vec[n + i] = l2;
       }
       __syncthreads();
-      if (tid == 0) {
-        tm[g + 1] = t1;
-        x1[g + 2] = T(1);
-      }
+      if (tid == 0) x1[g + 2] = T(1);
       // ---- X[s:, s:] -= wv l2^T - l2 wv^T -------------------------------------
       if (s0 < n) {
         // flattened strictly-lower trapezoid of the trailing block, column-major
@@ -266,7 +305,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
 
 template <typename T>
 size_t batched_smem(int n, int J0) {
-  size_t head = (2 * n * sizeof(T) + (kBWarps + 2 + n) * sizeof(int) + 15) & ~size_t(15);
+  size_t head = (kRedBytes + 2 * n * sizeof(T) + n * sizeof(int) + 15) & ~size_t(15);
   long long cols = 0;
   for (int j = J0; j < n - 1; ++j) cols += n - 1 - j;
   return head + (size_t)cols * sizeof(T);
