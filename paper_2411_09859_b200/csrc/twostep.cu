@@ -69,10 +69,12 @@ struct TCtx {
   int smem_mode;
   double* L;
   long long ldl;
-  __device__ double* col(int j) const {
+  int lgC;        // C is a power of two (8 or 16)
+  __device__ __forceinline__ double* col(int j) const {
     if (!smem_mode) return L + (long long)j * ldl;
-    double* p = local + (size_t)(j / C) * n;
-    return (j % C == cta) ? p : cl.map_shared_rank(p, j % C);
+    double* p = local + (size_t)(j >> lgC) * n;
+    const int owner = j & (C - 1);
+    return owner == cta ? p : cl.map_shared_rank(p, owner);
   }
 };
 
@@ -163,7 +165,8 @@ __device__ void sym_swap(const TCtx& c, int a, int b) {
 
 __global__ void __launch_bounds__(kTThreads, 1) twostep_kernel(TArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  TCtx c{cg::this_cluster(), nullptr, (int)gridDim.x, (int)blockIdx.x, a.n, a.smem_mode, a.L, a.ldl};
+  TCtx c{cg::this_cluster(), nullptr, (int)gridDim.x, (int)blockIdx.x, a.n, a.smem_mode, a.L, a.ldl,
+         gridDim.x == 16 ? 4 : (gridDim.x == 8 ? 3 : (gridDim.x == 4 ? 2 : (gridDim.x == 2 ? 1 : 0)))};
   const int n = a.n, C = c.C, cta = c.cta, tid = threadIdx.x;
   const int ncl = (n + C - 1) / C;
   double* vbuf = reinterpret_cast<double*>(smem_raw);  // [2][n] staged wv, l2
