@@ -25,17 +25,77 @@ namespace skl {
 
 namespace {
 
-constexpr int kStages = 4;
-constexpr int kK4PerStage = 4;                    // 16 k per stage
+#ifndef SKL_GEMM_STAGES
+#define SKL_GEMM_STAGES 3
+#define SKL_GEMM_K4_PER_STAGE 4
+#endif
+#ifndef SKL_GEMM_NOPF
+#define SKL_GEMM_NOPF 0
+#endif
+#ifndef SKL_GEMM_NOEPI
+#define SKL_GEMM_NOEPI 0
+#endif
+#ifndef SKL_GEMM_FIXNB
+#define SKL_GEMM_FIXNB 0
+#endif
+#ifndef SKL_GEMM_HINTS
+#define SKL_GEMM_HINTS 0
+#endif
+constexpr int kStages = SKL_GEMM_STAGES;
+constexpr int kK4PerStage = SKL_GEMM_K4_PER_STAGE;  // 4*kK4PerStage k per stage
 constexpr int kBlkDoubles = 16 * 32;              // one k4 block of a 128-row tile
 constexpr int kStageDoubles = kK4PerStage * kBlkDoubles;
 constexpr int kGemmThreads = 256;
-constexpr size_t kGemmSmem = size_t(kStages) * 2 * kStageDoubles * sizeof(double) + 64;
+constexpr int kGemmWarps = kGemmThreads / 32;
+// C staging buffer of the bulk-reduce epilogue: 128 columns of 128 rows, column
+// stride 130 doubles (1040 B: 16-byte aligned for the bulk engine, and a warp's
+// fragment store of four column pairs lands on disjoint bank halves -> 2 wavefronts)
+constexpr int kCbStride = 130;
+constexpr size_t kRingBytes = size_t(kStages) * 2 * kStageDoubles * sizeof(double);
+constexpr size_t kCbufBytes = size_t(kTile) * kCbStride * sizeof(double);
+constexpr size_t kGemmSmem = kRingBytes + kCbufBytes + 2 * kStages * sizeof(uint64_t);
+static_assert(kGemmSmem <= 232448, "GEMM shared memory exceeds the sm_100 opt-in limit");
 
 __device__ __forceinline__ size_t packed_off(int row, int col, int k4cap) {
   int t = row >> 7, mb = (row >> 3) & 15, r8 = row & 7;
   int q = col >> 2, c4 = col & 3;
   return (((size_t)t * k4cap + q) * 16 + mb) * 32 + (r8 * 4 + c4);
+}
+
+// Tile raster: bands of kBand tile-rows; inside a band, columns ascend and rows
+// ascend within a column.  The ~148 tiles in flight at once then span ~kBand P
+// tiles and ~148/kBand Q tiles, so no packed operand tile is read by every SM
+// at the same moment (a plain row-major walk has all SMs on one P tile, which
+// hot-spots the L2 slices holding it).
+#ifndef SKL_GEMM_BAND
+#define SKL_GEMM_BAND 8
+#endif
+constexpr int kBand = SKL_GEMM_BAND;
+__host__ __device__ __forceinline__ void lower_tile_swizzled(int t, int nt, int& ti, int& tj) {
+  // full band b holds G^2 b + G(G+1)/2 tiles; cum(b) = G^2 b(b-1)/2 + b G(G+1)/2
+  constexpr long long G = kBand;
+  auto cum = [](long long b) { return G * G * b * (b - 1) / 2 + b * G * (G + 1) / 2; };
+  const float a = 0.5f * G * G, bb = 0.5f * G * (G + 1) - 0.5f * G * G;
+  long long b = (long long)((-bb + sqrtf(bb * bb + 4.f * a * (float)t)) / (2.f * a));
+  if (b < 0) b = 0;
+  while (b > 0 && cum(b) > t) --b;
+  while (cum(b + 1) <= t) ++b;
+  const int r0 = int(b * G);
+  const int h = min(int(G), nt - r0);
+  int u = int(t - cum(b));
+  if (u < h * r0) {
+    tj = u / h;
+    ti = r0 + (u - tj * h);
+    return;
+  }
+  u -= h * r0;
+  int j = 0;
+  while (u >= h - j) {
+    u -= h - j;
+    ++j;
+  }
+  tj = r0 + j;
+  ti = tj + u;
 }
 
 // Persistent lower-triangular DGEMM-NT: one CTA per SM walks the lower tiles
@@ -49,7 +109,13 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sP = reinterpret_cast<double*>(smem_raw);
   double* sQ = sP + kStages * kStageDoubles;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + kStages * kStageDoubles);
+  double* cbuf = sQ + kStages * kStageDoubles;
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + kTile * kCbStride);
+  uint64_t* empty = full + kStages;
+  // interior tiles (ti > tj, all 128 rows in range) with beta == 1 finish through
+  // the bulk engine: accumulators -> shared -> cp.reduce.async.bulk .add.f64
+  // into C, which overlaps the read-modify-write of C with the next tile's MMAs
+  const bool bulk_ok = beta == 1.0 && (ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
 
   const int nt = tiles_for(n);
   const int ntiles = nt * (nt + 1) / 2;
@@ -77,33 +143,45 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     return;
   }
 
-  auto tile_of = [&](int i, int& ti, int& tj) {
-    const int t = blockIdx.x + i * gridDim.x;
-    ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    while (ti * (ti + 1) / 2 > t) --ti;
-    tj = t - ti * (ti + 1) / 2;
-  };
-
+  auto tile_of = [&](int i, int& ti, int& tj) { lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj); };
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kGemmWarps);
+    }
     fence_mbar_init();
   }
   __syncthreads();
 
   // global chunk q -> (tile i = q / nchunks, chunk c = q % nchunks)
+  // producer state (tid 0): chunks are issued strictly in order, so the tile
+  // coordinates are recomputed only when the issue cursor enters a new tile --
+  // the per-chunk cost stays a few integer ops on warp 0's critical path
+  int iss_q = 0, iss_i = -1, iss_c = 0, iss_ti = 0, iss_tj = 0;
   auto issue = [&](int q) {
-    const int s = q % kStages;
-    const int i = q / nchunks, c = q - i * nchunks;
-    int ti, tj;
-    tile_of(i, ti, tj);
-    const int q0 = c * kK4PerStage;
+    (void)q;  // == iss_q
+    if (iss_i < 0 || iss_c == nchunks) {
+      ++iss_i;
+      iss_c = 0;
+      tile_of(iss_i, iss_ti, iss_tj);
+    }
+    const int s = iss_q % kStages;
+    const int q0 = iss_c * kK4PerStage;
     const int nb = min(kK4PerStage, nk4 - q0);
     const uint32_t bytes = uint32_t(nb) * kBlkDoubles * sizeof(double);
     mbar_arrive_expect_tx(&full[s], 2 * bytes);
-    bulk_g2s(sP + s * kStageDoubles, P + ((size_t)ti * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
-    bulk_g2s(sQ + s * kStageDoubles, Q + ((size_t)tj * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
+#if SKL_GEMM_HINTS
+    const uint64_t pol = l2_policy_evict_last();  // packed operands are re-read by many tiles
+    bulk_g2s_hint(sP + s * kStageDoubles, P + ((size_t)iss_ti * k4cap + q0) * kBlkDoubles, bytes, &full[s], pol);
+    bulk_g2s_hint(sQ + s * kStageDoubles, Q + ((size_t)iss_tj * k4cap + q0) * kBlkDoubles, bytes, &full[s], pol);
+#else
+    bulk_g2s(sP + s * kStageDoubles, P + ((size_t)iss_ti * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
+    bulk_g2s(sQ + s * kStageDoubles, Q + ((size_t)iss_tj * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
+#endif
+    ++iss_q;
+    ++iss_c;
   };
+
   if (tid == 0) {
     for (int q = 0; q < min(kStages, total_chunks); ++q) issue(q);
   }
@@ -113,7 +191,7 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     int ti, tj;
     tile_of(i, ti, tj);
     // warm L2 with this tile's C columns (read-modify-written in the epilogue)
-    if (tid < kTile) {
+    if (!SKL_GEMM_NOPF && tid < kTile) {
       const int col = tj * kTile + tid;
       const int r0 = ti * kTile;
       if (col < n && r0 < n) {
@@ -133,7 +211,7 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     for (int c = 0; c < nchunks; ++c, ++q) {
       const int s = q % kStages;
       mbar_wait(&full[s], (q / kStages) & 1);
-      const int nb = min(kK4PerStage, nk4 - c * kK4PerStage);
+      const int nb = SKL_GEMM_FIXNB ? kK4PerStage : min(kK4PerStage, nk4 - c * kK4PerStage);
       const double* ps = sP + s * kStageDoubles + (wm * 8) * 32 + lane;
       const double* qs = sQ + s * kStageDoubles + (wn * 4) * 32 + lane;
       for (int kb = 0; kb < nb; ++kb) {
@@ -147,11 +225,51 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
       }
-      __syncthreads();  // every warp is done with stage s
-      if (tid == 0 && q + kStages < total_chunks) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done reading stage s
+      // refill the stage the PREVIOUS chunk used: the other warps are at most a
+      // chunk behind warp 0, so the wait is short and stalls only warp 0
+      if (tid == 0 && q >= 1 && q - 1 + kStages < total_chunks) {
+        const int qp = q - 1;
+        mbar_wait(&empty[qp % kStages], (qp / kStages) & 1);
         fence_proxy_async();
-        issue(q + kStages);
+        issue(qp + kStages);
       }
+    }
+
+    if (SKL_GEMM_NOEPI) {
+      double sum = 0.0;
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) sum += acc[mi][ni][0] + acc[mi][ni][1];
+      if (sum == 1234.5) C[0] = sum;
+      continue;
+    }
+    if (bulk_ok && ti > tj && (ti + 1) * kTile <= n) {
+      // warp-local: this warp's 64x32 block goes through its own slice of cbuf
+      // (lane l owns column wn*32+l), so no CTA barrier and warps drift freely
+      bulk_wait_read0();  // this lane's reduce of the previous tile has drained
+      __syncwarp();
+      double* cb = cbuf + (wn * 32 + 2 * (lane & 3)) * kCbStride + wm * 64 + (lane >> 2);
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) cb[(ni * 8 + e) * kCbStride + mi * 8] = acc[mi][ni][e];
+      fence_proxy_async();
+      __syncwarp();
+      const int col = wn * 32 + lane;
+#if SKL_GEMM_HINTS
+      bulk_reduce_add_f64_hint(C + (long long)(tj * kTile + col) * ldc + ti * kTile + wm * 64,
+                               cbuf + col * kCbStride + wm * 64, 64 * sizeof(double), l2_policy_evict_first());
+#else
+      bulk_reduce_add_f64(C + (long long)(tj * kTile + col) * ldc + ti * kTile + wm * 64, cbuf + col * kCbStride + wm * 64,
+                          64 * sizeof(double));
+#endif
+      bulk_commit();
+      continue;
     }
 
     const int row_base = ti * kTile + wm * 64 + (lane >> 2);
@@ -182,6 +300,7 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
           }
     }
   }
+  bulk_wait0();
 }
 
 __device__ __forceinline__ void packed_decode(size_t off, int k4cap, int& row, int& col) {
