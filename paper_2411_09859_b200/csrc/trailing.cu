@@ -18,6 +18,9 @@
 // Only lower tiles are launched (triangle-aware schedule); diagonal tiles
 // mask i <= j at load and store, so the upper triangle is never read or
 // written (test_core.py:39-58 NaN-poison invariant).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -29,31 +32,20 @@ namespace {
 #define SKL_GEMM_STAGES 3
 #define SKL_GEMM_K4_PER_STAGE 4
 #endif
-#ifndef SKL_GEMM_NOPF
-#define SKL_GEMM_NOPF 0
-#endif
-#ifndef SKL_GEMM_NOEPI
-#define SKL_GEMM_NOEPI 0
-#endif
-#ifndef SKL_GEMM_FIXNB
-#define SKL_GEMM_FIXNB 0
-#endif
-#ifndef SKL_GEMM_HINTS
-#define SKL_GEMM_HINTS 0
-#endif
 constexpr int kStages = SKL_GEMM_STAGES;
 constexpr int kK4PerStage = SKL_GEMM_K4_PER_STAGE;  // 4*kK4PerStage k per stage
 constexpr int kBlkDoubles = 16 * 32;              // one k4 block of a 128-row tile
 constexpr int kStageDoubles = kK4PerStage * kBlkDoubles;
 constexpr int kGemmThreads = 256;
 constexpr int kGemmWarps = kGemmThreads / 32;
-// C staging buffer of the bulk-reduce epilogue: 128 columns of 128 rows, column
-// stride 130 doubles (1040 B: 16-byte aligned for the bulk engine, and a warp's
-// fragment store of four column pairs lands on disjoint bank halves -> 2 wavefronts)
-constexpr int kCbStride = 130;
+// C staging of the tensor-reduce epilogue: per warp, its 64x32 block as four
+// 16-row x 32-col boxes (4 KiB each, 128-byte swizzled, 1 KiB aligned) that
+// cp.reduce.async.bulk.tensor adds into C through a tensor map.
+constexpr int kBoxRows = 16, kBoxCols = 32;
+constexpr int kBoxDoubles = kBoxRows * kBoxCols;
 constexpr size_t kRingBytes = size_t(kStages) * 2 * kStageDoubles * sizeof(double);
-constexpr size_t kCbufBytes = size_t(kTile) * kCbStride * sizeof(double);
-constexpr size_t kGemmSmem = kRingBytes + kCbufBytes + 2 * kStages * sizeof(uint64_t);
+constexpr size_t kCbufBytes = size_t(kGemmWarps) * 4 * kBoxDoubles * sizeof(double);
+constexpr size_t kGemmSmem = 1024 + kRingBytes + kCbufBytes + 2 * kStages * sizeof(uint64_t);
 static_assert(kGemmSmem <= 232448, "GEMM shared memory exceeds the sm_100 opt-in limit");
 
 __device__ __forceinline__ size_t packed_off(int row, int col, int k4cap) {
@@ -104,19 +96,22 @@ __host__ __device__ __forceinline__ void lower_tile_swizzled(int t, int nt, int&
 // C tile is prefetched into L2 when a tile starts and read-modified-written
 // in the epilogue (accumulators start at zero).
 __global__ void __launch_bounds__(kGemmThreads, 1)
-gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q, int k4cap, int nk4_host,
+gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, const double* __restrict__ P,
+                     const double* __restrict__ Q, int k4cap, int nk4_host,
                      const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sP = reinterpret_cast<double*>(smem_raw);
+  // 1 KiB-align the carve-up (the swizzled boxes need it)
+  unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* sP = reinterpret_cast<double*>(smem_al);
   double* sQ = sP + kStages * kStageDoubles;
   double* cbuf = sQ + kStages * kStageDoubles;
-  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + kTile * kCbStride);
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + kGemmWarps * 4 * kBoxDoubles);
   uint64_t* empty = full + kStages;
-  // interior tiles (ti > tj, all 128 rows in range) with beta == 1 finish through
-  // the bulk engine: accumulators -> shared -> cp.reduce.async.bulk .add.f64
-  // into C, which overlaps the read-modify-write of C with the next tile's MMAs
-  const bool bulk_ok = beta == 1.0 && (ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
-
+  // off-diagonal tiles with beta == 1 finish through the bulk engine: accumulators
+  // -> swizzled shared boxes -> cp.reduce.async.bulk.tensor .add into C (rows
+  // past n clipped by the tensor map), overlapping C's read-modify-write with
+  // the next tile's MMAs; diagonal tiles keep the masked register epilogue
+  const bool bulk_ok = use_tmap && beta == 1.0;
   const int nt = tiles_for(n);
   const int ntiles = nt * (nt + 1) / 2;
   const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
@@ -170,14 +165,8 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     const int nb = min(kK4PerStage, nk4 - q0);
     const uint32_t bytes = uint32_t(nb) * kBlkDoubles * sizeof(double);
     mbar_arrive_expect_tx(&full[s], 2 * bytes);
-#if SKL_GEMM_HINTS
-    const uint64_t pol = l2_policy_evict_last();  // packed operands are re-read by many tiles
-    bulk_g2s_hint(sP + s * kStageDoubles, P + ((size_t)iss_ti * k4cap + q0) * kBlkDoubles, bytes, &full[s], pol);
-    bulk_g2s_hint(sQ + s * kStageDoubles, Q + ((size_t)iss_tj * k4cap + q0) * kBlkDoubles, bytes, &full[s], pol);
-#else
     bulk_g2s(sP + s * kStageDoubles, P + ((size_t)iss_ti * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
     bulk_g2s(sQ + s * kStageDoubles, Q + ((size_t)iss_tj * k4cap + q0) * kBlkDoubles, bytes, &full[s]);
-#endif
     ++iss_q;
     ++iss_c;
   };
@@ -191,7 +180,7 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     int ti, tj;
     tile_of(i, ti, tj);
     // warm L2 with this tile's C columns (read-modify-written in the epilogue)
-    if (!SKL_GEMM_NOPF && tid < kTile) {
+    if (tid < kTile) {
       const int col = tj * kTile + tid;
       const int r0 = ti * kTile;
       if (col < n && r0 < n) {
@@ -211,7 +200,7 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     for (int c = 0; c < nchunks; ++c, ++q) {
       const int s = q % kStages;
       mbar_wait(&full[s], (q / kStages) & 1);
-      const int nb = SKL_GEMM_FIXNB ? kK4PerStage : min(kK4PerStage, nk4 - c * kK4PerStage);
+      const int nb = min(kK4PerStage, nk4 - c * kK4PerStage);
       const double* ps = sP + s * kStageDoubles + (wm * 8) * 32 + lane;
       const double* qs = sQ + s * kStageDoubles + (wn * 4) * 32 + lane;
       for (int kb = 0; kb < nb; ++kb) {
@@ -237,38 +226,33 @@ gemm_lower_nt_kernel(const double* __restrict__ P, const double* __restrict__ Q,
       }
     }
 
-    if (SKL_GEMM_NOEPI) {
-      double sum = 0.0;
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) sum += acc[mi][ni][0] + acc[mi][ni][1];
-      if (sum == 1234.5) C[0] = sum;
-      continue;
-    }
-    if (bulk_ok && ti > tj && (ti + 1) * kTile <= n) {
-      // warp-local: this warp's 64x32 block goes through its own slice of cbuf
-      // (lane l owns column wn*32+l), so no CTA barrier and warps drift freely
-      bulk_wait_read0();  // this lane's reduce of the previous tile has drained
+    if (bulk_ok && ti > tj) {
+      // warp-local: the warp's boxes are private, so no CTA barrier; lane 0
+      // issued this warp's previous reduces and waits for them to drain
+      bulk_wait_read0();
       __syncwarp();
-      double* cb = cbuf + (wn * 32 + 2 * (lane & 3)) * kCbStride + wm * 64 + (lane >> 2);
+      double* wbuf = cbuf + warp * 4 * kBoxDoubles;
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) cb[(ni * 8 + e) * kCbStride + mi * 8] = acc[mi][ni][e];
+          for (int e = 0; e < 2; ++e) {
+            // element (row, col) of the warp block -> box mi/2, 16-byte chunk
+            // (row%16)/2 XOR col%8 of the box's 128-byte column (SWIZZLE_128B)
+            const int r = (mi & 1) * 8 + (lane >> 2), col = ni * 8 + 2 * (lane & 3) + e;
+            wbuf[(mi >> 1) * kBoxDoubles + col * kBoxRows + (((r >> 1) ^ (col & 7)) << 1) + (r & 1)] =
+                acc[mi][ni][e];
+          }
       fence_proxy_async();
       __syncwarp();
-      const int col = wn * 32 + lane;
-#if SKL_GEMM_HINTS
-      bulk_reduce_add_f64_hint(C + (long long)(tj * kTile + col) * ldc + ti * kTile + wm * 64,
-                               cbuf + col * kCbStride + wm * 64, 64 * sizeof(double), l2_policy_evict_first());
-#else
-      bulk_reduce_add_f64(C + (long long)(tj * kTile + col) * ldc + ti * kTile + wm * 64, cbuf + col * kCbStride + wm * 64,
-                          64 * sizeof(double));
-#endif
-      bulk_commit();
+      if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          tensor_reduce_add_2d(&cmap, ti * kTile + wm * 64 + b * kBoxRows, tj * kTile + wn * 32,
+                               wbuf + b * kBoxDoubles);
+        bulk_commit();
+      }
       continue;
     }
 
@@ -455,6 +439,22 @@ int grid_for(size_t total, int threads) {
 
 }  // namespace
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      enc = nullptr;
+  }
+  return enc;
+}
+}  // namespace
+
 cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
                               double* C, long long ldc, int n, double beta, cudaStream_t stream) {
   if (n < 2) return cudaSuccess;
@@ -471,10 +471,25 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
+  // tensor map over C (rows x cols = n x n, column stride ldc) for the
+  // bulk-reduce epilogue; needs a 16-byte aligned base and an even ldc
+  CUtensorMap cmap;
+  memset(&cmap, 0, sizeof(cmap));
+  int use_tmap = 0;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
+  if (enc && beta == 1.0 && (ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)ldc * sizeof(double)};
+    cuuint32_t box[2] = {(cuuint32_t)kBoxRows, (cuuint32_t)kBoxCols}, es[2] = {1, 1};
+    use_tmap = enc(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   int nt = tiles_for(n);
   int ntiles = nt * (nt + 1) / 2;
   int grid = ntiles < nsm ? ntiles : nsm;
-  gemm_lower_nt_kernel<<<grid, kGemmThreads, kGemmSmem, stream>>>(P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta);
+  gemm_lower_nt_kernel<<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc,
+                                                                  n, beta);
   return cudaGetLastError();
 }
 
