@@ -195,6 +195,7 @@ __device__ __forceinline__ void compute_az(const CSmem& s, int Rs, int R, int rc
 template <bool MULTI>
 __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const long long t_kernel0 = clock64();
   cg::cluster_group cluster = cg::this_cluster();
   const int C = MULTI ? int(cluster.num_blocks()) : int(gridDim.x);
   const int crank = MULTI ? int(cluster.block_rank()) : int(blockIdx.x);  // rank inside the cluster
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   cluster_barrier();
   long long pt[6] = {0, 0, 0, 0, 0, 0};
   long long t_prev = clock64();
+  const long long t_loop0 = t_prev;
 #define CMARK(i)                    \
   do {                              \
     long long _t = clock64();       \
@@ -547,8 +549,10 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     }
   }
   if (a.prof && tid == 0) {
-    for (int i = 0; i < 6; ++i) a.prof[cta * 8 + i] += (unsigned long long)pt[i];
-    a.prof[cta * 8 + 6] += (unsigned long long)(rt - r);
+    for (int i = 0; i < 6; ++i) a.prof[cta * 16 + i] += (unsigned long long)pt[i];
+    a.prof[cta * 16 + 6] += (unsigned long long)(rt - r);
+    a.prof[cta * 16 + 8] += (unsigned long long)(t_loop0 - t_kernel0);
+    a.prof[cta * 16 + 9] += (unsigned long long)(clock64() - t_prev);
   }
   if (a.want_y) {
 #pragma unroll
@@ -577,45 +581,31 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   if (cta == 0) {
     for (int i = tid; i < row0; i += kCThreads) a.gperm[i] = i;
   }
-  if (MULTI) {
-    // the slab goes to the panel buffer; panel_finish_* (separate launches, a grid-wide
-    // ordering point) materialise the displaced lines and write the L columns
-    for (int j = 0; j < kmax; ++j) {
-      const double* sc = s.slab + (size_t)j * Rs;
-      for (int li = tid; li < rcount; li += kCThreads) a.pbuf[(size_t)j * n + rbase + li] = sc[li];
+  const long long t_tail1 = clock64();
+  {
+    // the slab goes to the panel buffer; panel_finish_* (separate grid-wide launches,
+    // also the ordering point) materialise the displaced lines and write the L
+    // columns with every SM instead of this kernel's 16: the displaced lines are
+    // row accesses of column-major storage (one sector per element)
+    for (int li = tid; li < rcount; li += kCThreads) {
+      double* dst = a.pbuf + rbase + li;
+      int j = 0;
+      for (; j + 8 <= kmax; j += 8) {  // 8 loads in flight, then 8 streaming stores
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = s.slab[(size_t)(j + u) * Rs + li];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) __stcs(dst + (size_t)(j + u) * n, v[u]);
+      }
+      for (; j < kmax; ++j) __stcs(dst + (size_t)j * n, s.slab[(size_t)j * Rs + li]);
+    }
+    if (a.prof && tid == 0) {
+      const long long t_end = clock64();
+      a.prof[cta * 16 + 7] += (unsigned long long)(t_end - t_kernel0);
+      a.prof[cta * 16 + 10] += (unsigned long long)(t_tail1 - t_kernel0);
+      a.prof[cta * 16 + 11] += (unsigned long long)(t_end - t_tail1);
     }
     return;
-  }
-  __threadfence();
-  cluster_barrier();
-  const int nd = *((volatile int*)a.disp_count);
-  const int ntr = n - rt;
-  for (int q = cta; q < nd; q += C) {
-    const int p = a.disp_list[q];
-    const int pp = a.gperm[p];
-    double* line = a.side + (size_t)q * ntr;
-    for (int i = rt + tid; i < n; i += kCThreads) line[i - rt] = (i == p) ? 0.0 : skew_at(W, ld, a.gperm[i], pp);
-  }
-  __threadfence();
-  cluster_barrier();
-  for (int j = 0; j < kmax; ++j) {
-    const int c = lo + j;
-    const double* sc = s.slab + (size_t)j * Rs;
-    for (int li = tid; li < rcount; li += kCThreads) {
-      int pos = rbase + li;
-      if (pos > c) W[(long long)c * ld + pos] = sc[li];
-    }
-  }
-  for (int q = cta; q < nd; q += C) {
-    const int p = a.disp_list[q];
-    const double* line = a.side + (size_t)q * ntr;
-    for (int i = rt + tid; i < n; i += kCThreads) {
-      double v = line[i - rt];
-      if (i > p)
-        W[(long long)p * ld + i] = v;
-      else if (i < p)
-        W[(long long)i * ld + p] = -v;
-    }
   }
 }
 
@@ -655,6 +645,20 @@ __global__ void panel_finish_write(PanelArgs a) {
   }
 }
 
+
+// displaced trailing lines -> side buffer, then panel buffer -> L columns and
+// side -> trailing lines (two launches: the gather must see the pre-panel W)
+cudaError_t launch_panel_finish(const PanelArgs& a, cudaStream_t stream) {
+  const int ntr = a.n - (a.r + a.nelim);
+  dim3 grid(ntr > 0 ? (ntr + 255) / 256 : 1, 2 * (a.nelim + 1));
+  if (grid.x > 16) grid.x = 16;
+  panel_finish_gather<<<grid, 256, 0, stream>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 grid2(grid.x, a.kmax > 2 * (a.nelim + 1) ? a.kmax : 2 * (a.nelim + 1));
+  panel_finish_write<<<grid2, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
 
 }  // namespace
 
@@ -710,7 +714,9 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream) {
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, panel_cluster_kernel<false>, a);
+  e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel<false>, a);
+  if (e != cudaSuccess) return e;
+  return launch_panel_finish(a, stream);
 }
 
 // Largest number of co-resident clusters of size `csize` for a given smem size (0: none).
@@ -765,14 +771,7 @@ cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t strea
   cfg.numAttrs = 2;
   e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel<true>, a);
   if (e != cudaSuccess) return e;
-  const int ntr = a.n - (a.r + a.nelim);
-  dim3 grid(ntr > 0 ? (ntr + 255) / 256 : 1, 2 * (a.nelim + 1));
-  if (grid.x > 16) grid.x = 16;
-  panel_finish_gather<<<grid, 256, 0, stream>>>(a);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  dim3 grid2(grid.x, a.kmax > 2 * (a.nelim + 1) ? a.kmax : 2 * (a.nelim + 1));
-  panel_finish_write<<<grid2, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+  return launch_panel_finish(a, stream);
 }
 
 }  // namespace skl
