@@ -98,6 +98,22 @@ size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant);
 int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
                      double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Same factorization from HOST buffers (the drop-in call with H2D/D2H inside;
+ * X_host/L_host column-major, pinned for asynchronous copies).  Only the
+ * lower part travels: column blocks [j0, j0+128) move rows [j0, n), i.e. the
+ * strict lower triangle plus the 128x128 diagonal blocks.  L_host receives
+ * the reference's work buffer on those blocks (the factor with its explicit
+ * ones below the diagonal; X's values on/above the diagonal inside the
+ * diagonal blocks); the rest of L_host's upper triangle is not written (it is
+ * X's upper triangle in the reference's buffer: pass L_host == X_host, or a
+ * copy of X, for a bit-identical buffer).  tau_host (n-1), piv_host (n).
+ * workspace: device bytes from skl_ltlt_blk_piv_host_workspace_size.  The
+ * call is stream-ordered: outputs are valid after the stream synchronizes. */
+size_t skl_ltlt_blk_piv_host_workspace_size(int n, int nb, int variant);
+int skl_ltlt_blk_piv_host(int n, int nb, int variant, const double* X_host, long long ldx, double* L_host,
+                          long long ldl, double* tau_host, long long* piv_host, void* workspace,
+                          size_t workspace_bytes, void* stream);
+
 /* ltlt_unb_twostep (unblocked.py:229-240): Wimmer two-step, optional pivoting.
  *   Same output layout.  Unpivoted breakdown: *info_dev (device int) is set
  *   to the column + 1 (0 = success) — ZeroPivot(column) on the host.        */

@@ -10,6 +10,6 @@ from .core import (InvalidVariant, PermutationVector, PivotUnsupported, Singular
                    compose_permutation, form_s_splitting, invert_permutation, random_skew)
 from .instrument import FlopCounter  # noqa: F401
 from .blocked import (DEFAULT_BLOCK, FactorizationResult, Features, ltlt_blk_piv,  # noqa: F401
-                      ltlt_blk_piv_device)
+                      ltlt_blk_piv_device, ltlt_blk_piv_host)
 
 __version__ = "0.1.0"

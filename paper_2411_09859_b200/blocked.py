@@ -84,6 +84,48 @@ def ltlt_blk_piv_device(x, b=DEFAULT_BLOCK, fused="var1", out=None, stream=None)
     return L, tau, piv
 
 
+def ltlt_blk_piv_host(x, b=DEFAULT_BLOCK, fused="var1", out=None, stream=None, sync=True):
+    """Host-buffer entry (``skl_ltlt_blk_piv_host``): H2D of X's lower part,
+    factorization, D2H of L's lower part, tau and piv in one stream-ordered call.
+
+    ``x`` is an F-ordered float64 numpy array (a view of pinned memory for
+    asynchronous copies).  ``out = (L, tau, piv)`` numpy arrays (L F-ordered,
+    may be ``x`` for an in-place factorization) are written: L's strict lower
+    triangle and its 128x128 diagonal blocks (see the header); the rest of
+    L's upper triangle is left untouched.  Returns ``(L, tau, piv)``.
+    """
+    if fused not in PIVOTED_FUSED:
+        raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
+    _check_block(b)
+    x = np.asarray(x)
+    if x.dtype != np.float64 or x.ndim != 2 or x.shape[0] != x.shape[1] or not x.flags.f_contiguous:
+        raise ValueError("x must be a square F-ordered float64 array")
+    m = x.shape[0]
+    if m < 1:
+        raise ValueError("m >= 1 required")
+    if out is None:
+        L = np.zeros((m, m), dtype=np.float64, order="F")
+        tau = np.empty(max(m - 1, 0), dtype=np.float64)
+        piv = np.empty(m, dtype=np.int64)
+    else:
+        L, tau, piv = out
+        if not (L.flags.f_contiguous and L.dtype == np.float64 and L.shape == (m, m)):
+            raise ValueError("out L must be an F-ordered float64 (m, m) array")
+    lib = _capi.load()
+    code = _capi.VARIANT_CODES[fused]
+    nbytes = lib.skl_ltlt_blk_piv_host_workspace_size(m, int(b), code)
+    if nbytes == 0:
+        raise InvalidVariant("configuration not supported by the GPU panel kernel")
+    ws = dv.workspace(nbytes)
+    st = lib.skl_ltlt_blk_piv_host(m, int(b), code, x.ctypes.data, m, L.ctypes.data, m,
+                                   tau.ctypes.data if m > 1 else None, piv.ctypes.data, ws.data_ptr(), nbytes,
+                                   dv.stream_ptr(stream))
+    _capi.check(st, "ltlt_blk_piv_host")
+    if sync:
+        (stream if stream is not None else dv.require_cuda().cuda.current_stream()).synchronize()
+    return L, tau, piv
+
+
 def ltlt_blk_piv(x: SkewMatrixLower, b=DEFAULT_BLOCK, fused="var1", features=None) -> FactorizationResult:
     """Pivoted blocked right-looking factorization (blocked.py:303-363).
 

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -541,6 +542,59 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     g_kt.launches++;
     SKL_TRY(skl::launch_finalize_l(ws.W, ld, X, ldx, L, ldl, n, ws.col_group, ws.sigma_all, L != X ? 1 : 0, st));
   }
+  return SKL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer driver: [dXL (n*n) | tau (n) | piv (n) | blk workspace]
+namespace {
+constexpr int kHostBlock = 128;
+size_t host_ws_head(int n) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return al(sizeof(double) * (size_t)n * n) + al(sizeof(double) * n) + al(sizeof(long long) * n);
+}
+}  // namespace
+
+size_t skl_ltlt_blk_piv_host_workspace_size(int n, int nb, int variant) {
+  if (n < 1 || nb < 1) return 0;
+  size_t blk = skl_ltlt_blk_piv_workspace_size(n, nb, variant);
+  if (blk == 0 && n > 1) return 0;
+  return host_ws_head(n) + blk;
+}
+
+int skl_ltlt_blk_piv_host(int n, int nb, int variant, const double* X_host, long long ldx, double* L_host,
+                          long long ldl, double* tau_host, long long* piv_host, void* workspace,
+                          size_t workspace_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (variant < SKL_VAR1 || variant > SKL_VAR2B) return SKL_UNSUPPORTED;
+  if (n < 1 || nb < 1 || ldx < n || ldl < n || !X_host || !L_host || (n > 1 && !tau_host) || !piv_host)
+    return SKL_BAD_ARGUMENT;
+  const size_t need = skl_ltlt_blk_piv_host_workspace_size(n, nb, variant);
+  if (need == 0) return SKL_UNSUPPORTED;
+  if (workspace_bytes < need) return SKL_BAD_ARGUMENT;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  unsigned char* base = static_cast<unsigned char*>(workspace);
+  double* dXL = reinterpret_cast<double*>(base);
+  double* dtau = reinterpret_cast<double*>(base + al(sizeof(double) * (size_t)n * n));
+  long long* dpiv = reinterpret_cast<long long*>(base + al(sizeof(double) * (size_t)n * n) + al(sizeof(double) * n));
+  void* wsb = base + host_ws_head(n);
+  const size_t wsb_bytes = workspace_bytes - host_ws_head(n);
+  // lower trapezoid of X, one 2-D copy per 128-column block
+  for (int j0 = 0; j0 < n; j0 += kHostBlock) {
+    const int w = std::min(kHostBlock, n - j0);
+    SKL_TRY(cudaMemcpy2DAsync(dXL + (size_t)j0 * n + j0, sizeof(double) * n, X_host + (size_t)j0 * ldx + j0,
+                              sizeof(double) * ldx, sizeof(double) * (n - j0), w, cudaMemcpyHostToDevice, st));
+  }
+  // in place on the device (L == X): the diagonal blocks keep X's upper values
+  int rc = skl_ltlt_blk_piv(n, nb, variant, dXL, n, dXL, n, dtau, dpiv, wsb, wsb_bytes, stream);
+  if (rc != SKL_OK) return rc;
+  for (int j0 = 0; j0 < n; j0 += kHostBlock) {
+    const int w = std::min(kHostBlock, n - j0);
+    SKL_TRY(cudaMemcpy2DAsync(L_host + (size_t)j0 * ldl + j0, sizeof(double) * ldl, dXL + (size_t)j0 * n + j0,
+                              sizeof(double) * n, sizeof(double) * (n - j0), w, cudaMemcpyDeviceToHost, st));
+  }
+  if (n > 1) SKL_TRY(cudaMemcpyAsync(tau_host, dtau, sizeof(double) * (n - 1), cudaMemcpyDeviceToHost, st));
+  SKL_TRY(cudaMemcpyAsync(piv_host, dpiv, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
   return SKL_OK;
 }
 

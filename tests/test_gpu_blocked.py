@@ -170,3 +170,28 @@ def test_config3_golden(golden):
     S = torch.tril(L[:, : n - 1], -2)
     lr = rr + S @ rr[1:]
     assert np.allclose(lr.cpu().numpy(), g["lr"], rtol=1e-10 * n, atol=1e-10 * n)
+
+
+@pytest.mark.parametrize("n,b,fused", [(1, 4, "var1"), (2, 1, "var1"), (300, 32, "var2a"), (640, 64, "var1"),
+                                       (1000, 128, "var2b")])
+def test_host_buffer_entry(n, b, fused):
+    """skl_ltlt_blk_piv_host (pinned host in/out, lower-triangle copies) returns the
+    device path's factors bit for bit, and in place reproduces the full buffer."""
+    import torch
+    x = skew_lower(n, 7 * n + b)
+    x = np.asfortranarray(x)
+    x[np.triu_indices(n)] = np.nan        # upper triangle + diagonal never read
+    dev = pk().ltlt_blk_piv(pk().SkewMatrixLower(x), b=b, fused=fused)
+    xp = torch.empty((n, n), dtype=torch.float64).pin_memory().numpy().T
+    xp[...] = x
+    L, tau, piv = pk().ltlt_blk_piv_host(xp, b, fused)
+    assert np.array_equal(np.tril(L, -1), np.tril(dev.l.data, -1))
+    assert np.array_equal(tau, dev.t.tau) and np.array_equal(piv, dev.p.pivots)
+    # L's upper triangle: X's values inside the 128x128 diagonal blocks, untouched (0) elsewhere
+    for j in range(n):
+        blk0 = (j // 128) * 128
+        assert np.all(np.isnan(L[blk0:j + 1, j])) and not L[:blk0, j].any()
+    # in place: the whole buffer equals the reference's work buffer
+    L2, tau2, piv2 = pk().ltlt_blk_piv_host(xp, b, fused, out=(xp, np.empty(max(n - 1, 0)), np.empty(n, np.int64)))
+    assert L2 is xp and np.array_equal(np.tril(xp, -1), np.tril(dev.l.data, -1))
+    assert np.array_equal(np.isnan(np.triu(xp)), np.isnan(np.triu(x))) and np.array_equal(tau2, tau)

@@ -61,6 +61,31 @@ __global__ void __launch_bounds__(256, 1) xk(int K, int rounds, long long* out) 
       for (int j = tid; j < K; j += 256) wrow[j] = wr[j];
       __syncthreads();
       chk += wrow[K - 1] + cand[par][winner][0];
+    } else if (MODE == 4 || MODE == 5) {
+      // local publish: header + row into pub-like slot send[par][0]
+      if (warp == 0) {
+        for (int j = lane; j < K; j += 32) send[par][0][2 + j] = slab[(j & 1) * 256 + cand_row];
+        if (lane == 0) { send[par][0][0] = 1.0 + rank; send[par][0][1] = cand_row; }
+      } else if (MODE == 5 && warp == 1 && rank == owner_a) {
+        for (int j = lane; j < K + 1; j += 32) send[par][1][j] = slab[(j & 1) * 256 + (cand_row ^ 1)];
+      }
+      cbar();
+      const int L = K + 2;
+      const int tot = 16 * L + (MODE == 5 ? K + 1 : 0);
+#pragma unroll 4
+      for (int e = tid; e < tot; e += 256) {
+        double v;
+        if (e < 16 * L) {
+          const int m = e / L, j = e - m * L;
+          v = *cl.map_shared_rank(&send[par][0][j], m);
+          recv[par][m][j] = v;
+        } else {
+          v = *cl.map_shared_rank(&send[par][1][e - 16 * L], owner_a);
+          recv[par][16][e - 16 * L] = v;
+        }
+      }
+      __syncthreads();
+      chk += recv[par][winner][2 + K - 1] + recv[par][winner][0];
     } else if (MODE == 1 || MODE == 3) {
       const bool extra = MODE == 3 && rank == owner_a;
       if (tid == 0) {
@@ -128,10 +153,11 @@ int main() {
   long long* out;
   cudaMalloc(&out, 64 * 8);
   long long h[64];
-  void (*fns[4])(int, int, long long*) = {xk<0>, xk<1>, xk<2>, xk<3>};
-  const char* names[4] = {"pull+cbar", "bulk push", "st.async push", "bulk push+rowA"};
+  void (*fns[6])(int, int, long long*) = {xk<0>, xk<1>, xk<2>, xk<3>, xk<4>, xk<5>};
+  const char* names[6] = {"pull+cbar", "bulk push", "st.async push", "bulk push+rowA", "cbar+pull-all", "cbar+pull-all+rowA"};
   for (int K : {33, 65, 97, 129}) {
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < 6; ++m) {
+      if (m == 2) continue;
       cudaFuncSetAttribute(fns[m], cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(16);
