@@ -132,7 +132,8 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
     if (Rc <= 1024) {
       int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
       while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo) > smem_limit()) --w;
-      if (w >= 1 && w >= std::min(want, 64)) {
+      static int min_w = env_int("SKL_MIN_CLUSTER_W", 64);
+      if (w >= 1 && w >= std::min(want, min_w)) {
         p = PanelPlan{r, w, lo, C, Rc, r + w - lo, 1, C};
         return true;
       }
