@@ -23,9 +23,13 @@ from .ltlt import (  # noqa: F401
     eliminate,
     form_s_entries,
     form_w,
+    ltlt_blk,
     ltlt_blk_piv,
     ltlt_unb_ll,
+    ltlt_unb_panel,
+    ltlt_unb_rl,
     ltlt_unb_twostep,
+    skew_tridiag_gemm,
     l_dense,
     pfaffian,
     pfaffian_slog,

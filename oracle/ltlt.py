@@ -64,6 +64,7 @@ class OracleResult:
     tau: np.ndarray
     pivots: np.ndarray
     flops: dict = field(default_factory=dict)
+    first_column: np.ndarray = None
 
 
 # ----------------------------------------------------------------------------
@@ -370,6 +371,46 @@ def form_w(a, tau, fc=_NULL):
     return w
 
 
+def _pack_tb(tau, b, jc, j1, pc, p1):
+    """Rows [pc, p1) of T B for B-columns [jc, j1) (kernels3.py:226-236)."""
+    k = b.shape[0]
+    bp = np.zeros((p1 - pc, j1 - jc), dtype=b.dtype)
+    lo1 = max(pc, 1)
+    if lo1 < p1:
+        bp[lo1 - pc:, :] = tau[lo1 - 1:p1 - 1, None] * b[lo1 - 1:p1 - 1, jc:j1]
+    hi2 = min(p1, k - 1)
+    if hi2 > pc:
+        bp[:hi2 - pc, :] -= tau[pc:hi2, None] * b[pc + 1:hi2 + 1, jc:j1]
+    return bp
+
+
+def skew_tridiag_gemm(c, alpha, a, tau, b, tril=False, fc=_NULL):
+    """C += alpha A (T B) on a p x q block, beta = 1, fused packing
+    (kernels3.py:239-302); tril writes only row > col entries."""
+    p, k = a.shape
+    q = b.shape[1]
+    written = _lower_entries(min(p, q)) + max(p - q, 0) * q if tril else p * q
+    fc.add("level3", 2 * k * written + 4 * k * q)
+    if p == 0 or q == 0 or alpha == 0 or k == 0:
+        return
+    for jc in range(0, q, N_C):
+        j1 = min(jc + N_C, q)
+        row0 = jc if tril else 0
+        tiles = [(ic, min(ic + M_C, p)) for ic in range(row0, p, M_C)]
+        if not tiles:
+            continue
+        for pc, p1 in _k_panels(k):
+            bp = _pack_tb(tau, b, jc, j1, pc, p1)
+            ak = a[:, pc:p1]
+            for ic, i1 in tiles:
+                tile = c[ic:i1, jc:j1]
+                contrib = ak[ic:i1].dot(bp)
+                if not tril or ic >= j1:
+                    _accum_tile(tile, contrib, alpha)
+                else:
+                    _merge_tile(tile, contrib, alpha, ic - jc)
+
+
 # ----------------------------------------------------------------------------
 # unblocked.py restatements
 # ----------------------------------------------------------------------------
@@ -448,6 +489,73 @@ def panel_twostep(work, tau, base, nelim, climit, pivot=False, pivots=None,
         g += 2
 
 
+def panel_rl(work, tau, base, nelim, climit, pivot=False, pivots=None, swap_from=None, fc=_NULL):
+    """Right-looking eliminations of [base, base+nelim), rank-2 updates
+    restricted to columns < climit (unblocked.py:122-133)."""
+    if swap_from is None:
+        swap_from = base
+    for g in range(base, base + nelim):
+        eliminate(work, tau, g, pivot, pivots, swap_from, fc)
+        s = g + 2
+        trapezoid_rank2(work, s, climit, 1, work[s:, g], work[s:, g + 1], fc)
+
+
+def apply_pending(work, base, climit, fc=_NULL):
+    """Delayed coupling of the previous block (unblocked.py:174-179)."""
+    s = base + 1
+    trapezoid_rank2(work, s, climit, 1, work[s:, base - 1], work[s:, base], fc)
+
+
+def apply_first_column(work, first_column, fc=_NULL):
+    """Non-default first L column: its transform applied up front (unblocked.py:182-189)."""
+    m = work.shape[0]
+    fcvec = np.asarray(first_column)
+    if fcvec.shape != (m - 1,):
+        raise ValueError("first_column must have length m - 1")
+    fcvec = fcvec.astype(work.dtype, copy=True)
+    skew_rank2(work[1:, 1:], 1, fcvec, work[1:, 0], fc)
+    return fcvec
+
+
+def ltlt_unb_rl(x, pivot=False):
+    """Unblocked right-looking (modified Parlett-Reid) driver (unblocked.py:192-202)."""
+    work, tau = _workbuf(x)
+    m = work.shape[0]
+    pivots = np.zeros(m, dtype=np.int64) if pivot else np.zeros(0, dtype=np.int64)
+    fc = _Counter()
+    panel_rl(work, tau, 0, m - 1, m, pivot, pivots if pivot else None, 0, fc)
+    return OracleResult(work, tau, pivots, fc.as_dict())
+
+
+def ltlt_unb_panel(x, panel_width, variant="ll", pivot=False, first_column=None):
+    """First ``panel_width`` columns only (unblocked.py:243-275)."""
+    if variant not in ("ll", "rl", "twostep"):
+        raise ValueError(f"unknown panel variant {variant!r}")
+    if pivot and variant != "ll":
+        raise ValueError("a pivoted panel factorization must be left-looking")
+    if pivot and first_column is not None:
+        raise ValueError("first_column is only supported without pivoting")
+    work, tau = _workbuf(x)
+    m = work.shape[0]
+    nelim = min(panel_width, m - 1)
+    climit = min(panel_width, m)
+    pivots = np.zeros(m, dtype=np.int64) if pivot else None
+    fc = _Counter()
+    fcvec = apply_first_column(work, first_column, fc) if first_column is not None else None
+    fc.in_panel = True
+    if variant == "ll":
+        panel_ll(work, tau, 0, nelim, 0, pivot, pivots, 0, fc)
+    elif variant == "rl":
+        panel_rl(work, tau, 0, nelim, climit, fc=fc)
+    else:
+        panel_twostep(work, tau, 0, nelim, climit, fc=fc)
+    fc.in_panel = False
+    lbuf = np.zeros_like(work)
+    lbuf[:, :nelim] = work[:, :nelim]
+    ptrim = pivots[:nelim + 1] if pivots is not None else np.zeros(0, dtype=np.int64)
+    return OracleResult(lbuf, tau, ptrim, fc.as_dict(), fcvec)
+
+
 def ltlt_unb_twostep(x, pivot=False):
     """Unblocked two-step driver (unblocked.py:229-240)."""
     work, tau = _workbuf(x)
@@ -458,14 +566,17 @@ def ltlt_unb_twostep(x, pivot=False):
     return OracleResult(work, tau, pivots, fc.as_dict())
 
 
-def ltlt_unb_ll(x, pivot=False):
+def ltlt_unb_ll(x, pivot=False, first_column=None):
     """Unblocked left-looking (modified Aasen) driver (unblocked.py:205-226)."""
+    if pivot and first_column is not None:
+        raise ValueError("first_column is only supported without pivoting")
     work, tau = _workbuf(x)
     m = work.shape[0]
     pivots = np.zeros(m, dtype=np.int64) if pivot else np.zeros(0, dtype=np.int64)
     fc = _Counter()
+    fcvec = apply_first_column(work, first_column, fc) if first_column is not None else None
     panel_ll(work, tau, 0, m - 1, 0, pivot, pivots if pivot else None, 0, fc)
-    return OracleResult(work, tau, pivots, fc.as_dict())
+    return OracleResult(work, tau, pivots, fc.as_dict(), fcvec)
 
 
 # ----------------------------------------------------------------------------
@@ -543,6 +654,85 @@ def ltlt_blk_piv(x, b=DEFAULT_BLOCK, fused="var1"):
             pending = True
             r = rt
     return OracleResult(work, tau, pivots, fc.as_dict())
+
+
+def _panel_variant(work, tau, base, nelim, variant, carry, fc):
+    """_run_panel without pivoting (blocked.py:88-105)."""
+    climit = base + nelim
+    lo = base - 1 if carry else base
+    fc.in_panel = True
+    try:
+        if variant == "ll":
+            panel_ll(work, tau, base, nelim, lo, False, None, lo, fc)
+        elif variant == "rl":
+            if carry:
+                apply_pending(work, base, climit, fc)
+            panel_rl(work, tau, base, nelim, climit, fc=fc)
+        elif variant == "twostep":
+            if carry:
+                apply_pending(work, base, climit, fc)
+            panel_twostep(work, tau, base, nelim, climit, fc=fc)
+        else:
+            raise ValueError(f"unknown panel variant {variant!r}")
+    finally:
+        fc.in_panel = False
+
+
+def _couplings_rank2k(work, tau, c0, c1, region, fc):
+    """_apply_couplings(rank2k=True): W = A S then skew rank-2k (blocked.py:118-121)."""
+    m = work.shape[0]
+    if m - region < 2 or c1 - c0 < 1:
+        return
+    a = work[region:, c0 - 1:c1]
+    w = form_w(a, tau[c0:c1], fc)
+    skew_rank2k(work[region:, region:], 1, a, w, True, fc)
+
+
+def ltlt_blk(x, b=DEFAULT_BLOCK, driver="var1", panel_variant="ll"):
+    """Unpivoted blocked drivers (blocked.py:162-290): driver in var1, var2a,
+    var2b (right-looking), twostep (2a with W = A S + skew rank-2k), left
+    (left-looking: trapezoidal sandwiched gemm from the left, no trailing update)."""
+    if b < 1:
+        raise ValueError("block size must be >= 1")
+    work, tau = _workbuf(x)
+    m = work.shape[0]
+    fc = _Counter()
+    if driver == "var2b":
+        done, first = 0, True
+        while done < m - 1:
+            nelim = min(b + (1 if first else 0), m - 1 - done)
+            _panel_variant(work, tau, done, nelim, panel_variant, not first, fc)
+            new = done + nelim
+            _apply_couplings(work, tau, 1 if first else done, new, new, fc)
+            done, first = new, False
+    elif driver == "left":
+        r = 0
+        while r < m - 1:
+            be = min(b, m - 1 - r)
+            if r >= 2:
+                skew_tridiag_gemm(work[r:, r:r + be], -1, work[r:, 0:r], tau[1:r],
+                                  work[r:r + be, 0:r].T, True, fc)
+            _panel_variant(work, tau, r, be, panel_variant, r > 0, fc)
+            r += be
+    elif driver in ("var1", "var2a", "twostep"):
+        r, pending = 0, False
+        while r < m - 1:
+            be = min(b, m - 1 - r)
+            carry = driver != "var1" and pending
+            _panel_variant(work, tau, r, be, panel_variant, carry, fc)
+            rt = r + be
+            if driver == "var1":
+                _apply_couplings(work, tau, r + 1, rt, rt, fc)
+                _straggler(work, tau, rt, fc)
+            elif driver == "var2a":
+                _apply_couplings(work, tau, r if pending else r + 1, rt, rt, fc)
+            else:
+                _couplings_rank2k(work, tau, r if pending else r + 1, rt, rt, fc)
+            pending = True
+            r = rt
+    else:
+        raise ValueError(f"unknown driver {driver!r}")
+    return OracleResult(work, tau, np.zeros(0, dtype=np.int64), fc.as_dict())
 
 
 # ----------------------------------------------------------------------------

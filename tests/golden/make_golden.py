@@ -14,6 +14,10 @@ Fixtures
   cfg3_n16384_b256.npz (--big) same for config 3 (about 6 minutes of reference time)
   cfg4_batch.npz       (--big) pfaffian path per matrix (fp64 and fp32): sign, log|Pf| for all 8192,
                        pivots and tau for the first 128
+  unpiv_small.npz      unpivoted drivers: ltlt_blk_var1/2a/2b/twostep/left x panel
+                       variants ll/rl/twostep, ltlt_unb_rl (+pivoted), ltlt_unb_ll (+first_column),
+                       ltlt_unb_panel (ll/rl/twostep, pivoted, first_column) at n in {64, 150, 301}:
+                       tau, pivots, flops, L checksums (full strictly-lower L at n=64)
 """
 
 from __future__ import annotations
@@ -149,6 +153,38 @@ def main():
                     d[f"n{n}_b{b}_{fused}_{k}"] = v
         np.savez_compressed(HERE / "blk_small.npz", **d)
         print("small ok", flush=True)
+    if want("unpiv"):
+        d = {}
+
+        def put(key, r, n):
+            lr, ltr = checksums(r.l.data, n)
+            d[f"{key}_tau"] = r.t.tau
+            d[f"{key}_piv"] = r.p.pivots.astype(np.int32)
+            d[f"{key}_flops"] = flops_tuple(r.flops)
+            d[f"{key}_lr"], d[f"{key}_ltr"] = lr, ltr
+            if r.l.first_column is not None:
+                d[f"{key}_first"] = r.l.first_column
+            if n <= 64:
+                d[f"{key}_l"] = r.l.data[np.tril_indices(n, -1)]
+
+        for n, b in [(64, 16), (150, 32), (301, 64)]:
+            X = sk.SkewMatrixLower(skew_lower(n, n))
+            fcv = np.random.Generator(np.random.Philox(n)).standard_normal(n - 1) * 0.5
+            d[f"n{n}_first_column"] = fcv
+            for drv in ("var1", "var2a", "var2b", "twostep", "left"):
+                fn = getattr(sk, f"ltlt_blk_{drv}")
+                for pv in ("ll", "rl", "twostep"):
+                    put(f"n{n}_{drv}_{pv}", fn(X, b=b, panel_variant=pv), n)
+            put(f"n{n}_unb_rl", sk.ltlt_unb_rl(X), n)
+            put(f"n{n}_unb_rl_piv", sk.ltlt_unb_rl(X, pivot=True), n)
+            put(f"n{n}_unb_ll", sk.ltlt_unb_ll(X), n)
+            put(f"n{n}_unb_ll_first", sk.ltlt_unb_ll(X, first_column=fcv), n)
+            for pv in ("ll", "rl", "twostep"):
+                put(f"n{n}_panel40_{pv}", sk.ltlt_unb_panel(X, 40, variant=pv), n)
+            put(f"n{n}_panel40_piv", sk.ltlt_unb_panel(X, 40, pivot=True), n)
+            put(f"n{n}_panel40_first", sk.ltlt_unb_panel(X, 40, first_column=fcv), n)
+        np.savez_compressed(HERE / "unpiv_small.npz", **d)
+        print("unpiv ok", flush=True)
     if want("cfg2"):
         g = make_blk(sk, 4096, 128, "var1")
         for fused in ("var2a", "var2b"):

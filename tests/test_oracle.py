@@ -161,3 +161,65 @@ def test_residual_bound_small():
         x = skew_lower(n, 7)
         r = oracle.ltlt_blk_piv(x, b=32)
         assert oracle.residual(x, r.work, r.tau, r.pivots) <= 10 * EPS * n
+
+
+# ---- unpivoted drivers pinned to the reference ----------
+
+UNPIV_N = [(64, 16), (150, 32), (301, 64)]
+
+
+def unpiv_cases():
+    """(key suffix, oracle call) for every driver the unpiv fixture holds."""
+    out = []
+    for drv in ("var1", "var2a", "var2b", "twostep", "left"):
+        for pv in ("ll", "rl", "twostep"):
+            out.append((f"{drv}_{pv}", lambda x, b, fc, drv=drv, pv=pv: oracle.ltlt_blk(x, b, drv, pv)))
+    out += [
+        ("unb_rl", lambda x, b, fc: oracle.ltlt_unb_rl(x)),
+        ("unb_rl_piv", lambda x, b, fc: oracle.ltlt_unb_rl(x, True)),
+        ("unb_ll", lambda x, b, fc: oracle.ltlt_unb_ll(x)),
+        ("unb_ll_first", lambda x, b, fc: oracle.ltlt_unb_ll(x, first_column=fc)),
+        ("panel40_ll", lambda x, b, fc: oracle.ltlt_unb_panel(x, 40, "ll")),
+        ("panel40_rl", lambda x, b, fc: oracle.ltlt_unb_panel(x, 40, "rl")),
+        ("panel40_twostep", lambda x, b, fc: oracle.ltlt_unb_panel(x, 40, "twostep")),
+        ("panel40_piv", lambda x, b, fc: oracle.ltlt_unb_panel(x, 40, "ll", True)),
+        ("panel40_first", lambda x, b, fc: oracle.ltlt_unb_panel(x, 40, "ll", False, fc)),
+    ]
+    return out
+
+
+def l_checksum(work, n, seed=12345):
+    r = np.random.Generator(np.random.Philox(seed)).standard_normal(n)
+    S = np.tril(work[:, :n - 1], -2)
+    return r + S @ r[1:]
+
+
+@pytest.mark.parametrize("n,b", UNPIV_N)
+@pytest.mark.parametrize("case", unpiv_cases(), ids=lambda c: c[0])
+def test_unpivoted_drivers_fixture(golden, n, b, case):
+    """The oracle's unpivoted blocked / unblocked / panel drivers reproduce the
+    unmodified reference bit for bit (tau, pivots, flop tallies, L)."""
+    g = golden("unpiv_small.npz")
+    name, call = case
+    key = f"n{n}_{name}_"
+    r = call(skew_lower(n, n), b, g[f"n{n}_first_column"])
+    assert np.array_equal(r.tau, g[key + "tau"])
+    assert np.array_equal(r.pivots, g[key + "piv"])
+    assert [r.flops[k] for k in ("level2", "level3", "panel", "pivot")] == g[key + "flops"].tolist()
+    assert np.array_equal(l_checksum(r.work, n), g[key + "lr"])
+    if key + "first" in g:
+        assert np.array_equal(r.first_column, g[key + "first"])
+    if key + "l" in g:
+        assert np.array_equal(r.work[np.tril_indices(n, -1)], g[key + "l"])
+
+
+def test_unpivoted_zero_pivot_oracle():
+    """Unpivoted breakdown: exact zero pivot with a nonzero tail (unblocked.py:83-85)."""
+    x = np.zeros((4, 4), order="F")
+    x[2, 0], x[3, 1] = 1.0, 2.0          # X[1, 0] == 0, X[2, 0] != 0
+    with pytest.raises(ZeroDivisionError):
+        oracle.ltlt_blk(x, 2, "var2a")
+    z = np.zeros((3, 3), order="F")
+    z[2, 1] = 4.0                        # all-zero first column: tau 0, continue
+    r = oracle.ltlt_blk(z, 2, "var1")
+    assert r.tau.tolist() == [0.0, 4.0]
