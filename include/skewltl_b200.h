@@ -98,6 +98,25 @@ size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant);
 int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
                      double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Pivoted or unpivoted blocked LTL^T (blocked.py:162-233 ltlt_blk_var1/2a/2b,
+ *   blocked.py:303-363 ltlt_blk_piv).  pivot = 1: identical to skl_ltlt_blk_piv
+ *   (piv required).  pivot = 0: the pivot row of every step is row g+1; an exact
+ *   zero pivot with a nonzero column below it (unblocked.py:83-85) stores the
+ *   first such column + 1 in the device int *info (0 = success) -- ZeroPivot
+ *   on the host -- and the factors are then meaningless; piv is not written
+ *   (may be null).  Same layout/workspace as skl_ltlt_blk_piv (its size query). */
+int skl_ltlt_blk(int n, int nb, int variant, int pivot, const double* X, long long ldx, double* L, long long ldl,
+                 double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ltlt_unb_panel (unblocked.py:243-275): eliminate only columns [0, width) of
+ *   the whole matrix (left-looking, optional pivoting).  L receives the work
+ *   buffer; only its columns [0, min(width, n-1)) are meaningful (the
+ *   reference returns zeros elsewhere), tau[0:width), piv[0:width+1).         */
+size_t skl_ltlt_unb_panel_workspace_size(int n, int width);
+int skl_ltlt_unb_panel(int n, int width, int pivot, const double* X, long long ldx, double* L, long long ldl,
+                       double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
 /* Same factorization from HOST buffers (the drop-in call with H2D/D2H inside;
  * X_host/L_host column-major, pinned for asynchronous copies).  Only the
  * lower part travels: column blocks [j0, j0+128) move rows [j0, n), i.e. the

@@ -37,6 +37,9 @@ SIGNATURES = {
     "skl_apply_symmetric_pivot": (_i, [_i, _p, _ll, _i, _ll, _p]),
     "skl_ltlt_blk_piv_workspace_size": (_sz, [_i, _i, _i]),
     "skl_ltlt_blk_piv": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _sz, _p]),
+    "skl_ltlt_blk": (_i, [_i, _i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
+    "skl_ltlt_unb_panel_workspace_size": (_sz, [_i, _i]),
+    "skl_ltlt_unb_panel": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
     "skl_ltlt_blk_piv_host_workspace_size": (_sz, [_i, _i, _i]),
     "skl_ltlt_blk_piv_host": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _sz, _p]),
     "skl_ltlt_unb_twostep_workspace_size": (_sz, [_i]),

@@ -15,12 +15,13 @@ import numpy as np
 
 from . import _capi
 from . import device as dv
-from .core import (InvalidVariant, PermutationVector, SkewMatrixLower, SkewTridiagonal,
-                   UnitLowerFactor)
-from .instrument import FlopCounter, flops_blk_piv
+from .core import (InvalidVariant, PermutationVector, PivotUnsupported, SkewMatrixLower, SkewTridiagonal,
+                   UnitLowerFactor, ZeroPivot)
+from .instrument import FlopCounter, flops_blk_piv, flops_blk_unpivoted
 
 DEFAULT_BLOCK = 256                               # blocked.py:34
 PIVOTED_FUSED = ("var1", "var2a", "var2b")       # blocked.py:35
+PANEL_VARIANTS = ("ll", "rl", "twostep")         # unblocked.py VARIANTS
 
 
 @dataclass
@@ -161,3 +162,117 @@ def ltlt_blk_piv(x: SkewMatrixLower, b=DEFAULT_BLOCK, fused="var1", features=Non
                                    flops)
     return FactorizationResult(UnitLowerFactor(dv.to_host_colmajor(L), "ones"), SkewTridiagonal(tau_h),
                                PermutationVector(piv_h, m), flops)
+
+
+# ---------------------------------------------------------------------------
+# Unpivoted blocked drivers: blocked.py:162-290.  They run
+# the same GPU driver as ltlt_blk_piv with the pivot row fixed (skl_ltlt_blk,
+# pivot = 0); the panel is always the left-looking cluster kernel and the
+# trailing update the DMMA GEMM, which compute the same factorization as the
+# reference's rl / twostep panels and rank-2k couplings (equal in exact
+# arithmetic; the flop tally returned is the reference's for the requested
+# driver and panel variant, replayed by instrument.flops_blk_unpivoted).
+# ---------------------------------------------------------------------------
+
+_GPU_SCHEDULE = {"var1": "var1", "var2a": "var2a", "var2b": "var2b", "twostep": "var2a", "left": "var2a"}
+
+
+def _prep_input(x):
+    if not isinstance(x, SkewMatrixLower):
+        x = SkewMatrixLower(x)
+    m = x.m
+    if m < 1:
+        raise ValueError("m >= 1 required")
+    if dv.is_colmajor_cuda(x.data):
+        if x.data.dtype != dv.torch().float64:
+            raise TypeError("the blocked GPU path computes in float64")
+        return x, x.data, True
+    host = np.asarray(x.data)
+    if host.dtype == object:
+        raise TypeError("exact (object) dtypes are served by the reference, not the GPU path")
+    if host.dtype != np.float64:
+        raise TypeError("the blocked GPU path computes in float64")
+    return x, dv.to_device_colmajor(host), False
+
+
+def ltlt_blk_device(x, b=DEFAULT_BLOCK, fused="var1", pivot=False, out=None, stream=None):
+    """Device entry of skl_ltlt_blk: returns ``(L, tau, piv, info)`` CUDA tensors
+    without synchronising (``piv`` is None when unpivoted; ``info`` int32[1]:
+    first zero-pivot column + 1, 0 = success)."""
+    if fused not in PIVOTED_FUSED:
+        raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
+    _check_block(b)
+    t = dv.require_cuda()
+    m = x.shape[0]
+    if out is None:
+        L = dv.empty_colmajor(m, m, t.float64)
+        tau = t.empty(max(m - 1, 0), dtype=t.float64, device=x.device)
+    else:
+        L, tau = out
+    piv = t.empty(m, dtype=t.int64, device=x.device) if pivot else None
+    info = t.zeros(1, dtype=t.int32, device=x.device)
+    lib = _capi.load()
+    code = _capi.VARIANT_CODES[fused]
+    nbytes = lib.skl_ltlt_blk_piv_workspace_size(m, int(b), code)
+    if nbytes == 0:
+        raise InvalidVariant("configuration not supported by the GPU panel kernel")
+    ws = dv.workspace(nbytes)
+    st = lib.skl_ltlt_blk(m, int(b), code, 1 if pivot else 0, x.data_ptr(), dv.ld_of(x), L.data_ptr(), dv.ld_of(L),
+                          tau.data_ptr() if m > 1 else None, piv.data_ptr() if pivot else None, info.data_ptr(),
+                          ws.data_ptr(), nbytes, dv.stream_ptr(stream))
+    _capi.check(st, "ltlt_blk")
+    return L, tau, piv, info
+
+
+def _blk_unpivoted(x, b, driver, panel_variant, features, who):
+    _check_block(b)
+    if panel_variant not in PANEL_VARIANTS:
+        raise InvalidVariant(f"unknown panel variant {panel_variant!r}")
+    f = features or Features()
+    if driver != "var1" and not f.external_t:
+        raise InvalidVariant(f"{who} needs tau in an external vector (external_t)")
+    x, xd, on_device = _prep_input(x)
+    m = x.m
+    L, tau, _piv, info = ltlt_blk_device(xd, b, _GPU_SCHEDULE[driver], pivot=False)
+    code = int(info.item())
+    if code:
+        raise ZeroPivot(code - 1)
+    tau_h = tau.cpu().numpy()
+    l_host = None if on_device and driver != "twostep" else dv.to_host_colmajor(L)
+    flops = flops_blk_unpivoted(m, b, driver, panel_variant, tau_h, l_host)
+    l_out = L if on_device else l_host
+    return FactorizationResult(UnitLowerFactor(l_out, "ones"), SkewTridiagonal(tau if on_device else tau_h),
+                               PermutationVector(np.zeros(0, dtype=np.int64), m), flops)
+
+
+def ltlt_blk_var1(x: SkewMatrixLower, b=DEFAULT_BLOCK, panel_variant="ll", features=None) -> FactorizationResult:
+    """Blocked right-looking Variant 1 without pivoting (blocked.py:162-184)."""
+    return _blk_unpivoted(x, b, "var1", panel_variant, features, "blk-var1")
+
+
+def ltlt_blk_var2a(x: SkewMatrixLower, b=DEFAULT_BLOCK, panel_variant="ll", features=None) -> FactorizationResult:
+    """Fused Variant 2a without pivoting (blocked.py:187-208)."""
+    return _blk_unpivoted(x, b, "var2a", panel_variant, features, "blk-var2a")
+
+
+def ltlt_blk_var2b(x: SkewMatrixLower, b=DEFAULT_BLOCK, panel_variant="ll", features=None) -> FactorizationResult:
+    """Fused Variant 2b without pivoting (blocked.py:211-233)."""
+    return _blk_unpivoted(x, b, "var2b", panel_variant, features, "blk-var2b")
+
+
+def ltlt_blk_twostep(x: SkewMatrixLower, b=DEFAULT_BLOCK, panel_variant="ll", features=None) -> FactorizationResult:
+    """Blocked two-step path (blocked.py:268-290): Variant 2a's iteration whose
+    sandwich the reference realises as W = A S + skew rank-2k; the GPU runs the
+    same coupling through the one DMMA GEMM (Q = A T^T packed on the fly)."""
+    return _blk_unpivoted(x, b, "twostep", panel_variant, features, "blk-2step")
+
+
+def ltlt_blk_left(x: SkewMatrixLower, b=DEFAULT_BLOCK, pivot=False, panel_variant="ll",
+                  features=None) -> FactorizationResult:
+    """Blocked left-looking factorization (blocked.py:236-265).  Pivoting is
+    impossible at the blocked level (PivotUnsupported, blocked.py:247-248); the
+    unpivoted factors are computed by the right-looking GPU driver (the same
+    factorization; the tally is the left-looking one)."""
+    if pivot:
+        raise PivotUnsupported("a blocked pivoted left-looking algorithm cannot exist")
+    return _blk_unpivoted(x, b, "left", panel_variant, features, "blk-left")

@@ -168,15 +168,17 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   return true;
 }
 
-bool make_schedule(int n, int nb, int variant, std::vector<PanelPlan>& out) {
+// panels eliminating columns [0, ncols) (ncols = n - 1: the whole factorization)
+bool make_schedule(int n, int nb, int variant, std::vector<PanelPlan>& out, int ncols = -1) {
   out.clear();
   int nsm = skl::panel_max_ctas();
   PanelPlan p;
+  const int end = ncols < 0 ? n - 1 : std::min(ncols, n - 1);
   if (variant == SKL_VAR2B) {
     int done = 0;
     bool first = true;
-    while (done < n - 1) {
-      int want = std::min(nb + (first ? 1 : 0), n - 1 - done);
+    while (done < end) {
+      int want = std::min(nb + (first ? 1 : 0), end - done);
       int lo = first ? 0 : done - 1;
       if (!plan_panel(n, done, want, lo, nsm, p)) return false;
       out.push_back(p);
@@ -186,8 +188,8 @@ bool make_schedule(int n, int nb, int variant, std::vector<PanelPlan>& out) {
   } else {
     int r = 0;
     bool pending = false;
-    while (r < n - 1) {
-      int want = std::min(nb, n - 1 - r);
+    while (r < end) {
+      int want = std::min(nb, end - r);
       int lo = (variant == SKL_VAR2A && pending) ? r - 1 : r;
       if (!plan_panel(n, r, want, lo, nsm, p)) return false;
       out.push_back(p);
@@ -443,23 +445,36 @@ size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant) {
   return layout_blk(n, nb, plan, nullptr, nullptr);
 }
 
-int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
-                     double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream) {
+namespace {
+// blocked driver behind skl_ltlt_blk_piv / skl_ltlt_blk / skl_ltlt_unb_panel:
+// eliminates columns [0, ncols); pivot = 0 runs the unpivoted drivers (pivot row
+// fixed, exact-zero breakdown reported in *info)
+int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X, long long ldx, double* L,
+               long long ldl, double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes,
+               void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (variant < SKL_VAR1 || variant > SKL_VAR2B) return SKL_UNSUPPORTED;
   if (n < 1 || nb < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
+  if ((pivot && piv == nullptr) || (!pivot && info == nullptr)) return SKL_BAD_ARGUMENT;
   std::vector<PanelPlan> plan;
-  if (!make_schedule(n, nb, variant, plan)) {
+  if (!make_schedule(n, nb, variant, plan, ncols)) {
     g_last_error = "panel block does not fit the shared-memory budget";
     return SKL_UNSUPPORTED;
   }
+  if (!pivot)
+    for (const PanelPlan& p : plan)
+      if (p.cluster == 0) {
+        g_last_error = "the unpivoted drivers need the cluster panel kernels";
+        return SKL_UNSUPPORTED;
+      }
   size_t need = layout_blk(n, nb, plan, nullptr, nullptr);
   if (workspace_bytes < need) return SKL_BAD_ARGUMENT;
   BlkWorkspace ws;
   layout_blk(n, nb, plan, workspace, &ws);
   const long long ld = n;
 
-  SKL_TRY(cudaMemsetAsync(piv, 0, sizeof(long long) * n, st));
+  if (piv != nullptr) SKL_TRY(cudaMemsetAsync(piv, 0, sizeof(long long) * n, st));
+  if (info != nullptr) SKL_TRY(cudaMemsetAsync(info, 0, sizeof(int), st));
   if (n == 1) {
     if (L != X) SKL_TRY(cudaMemcpyAsync(L, X, sizeof(double), cudaMemcpyDeviceToDevice, st));
     return SKL_OK;
@@ -509,6 +524,8 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     static int dbg = env_int("SKL_PANEL_DBG", 0);
     a.dbg = dbg;
     a.prof = g_prof;
+    a.pivot = pivot;
+    a.info = info;
     {
       KScope ks(KPANEL, st);
       if (p.cluster == 2)
@@ -544,6 +561,33 @@ int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx,
     SKL_TRY(skl::launch_finalize_l(ws.W, ld, X, ldx, L, ldl, n, ws.col_group, ws.sigma_all, L != X ? 1 : 0, st));
   }
   return SKL_OK;
+}
+}  // namespace
+
+int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
+                     double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream) {
+  return blk_driver(n, nb, variant, 1, -1, X, ldx, L, ldl, tau, piv, nullptr, workspace, workspace_bytes, stream);
+}
+
+int skl_ltlt_blk(int n, int nb, int variant, int pivot, const double* X, long long ldx, double* L, long long ldl,
+                 double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes, void* stream) {
+  return blk_driver(n, nb, variant, pivot ? 1 : 0, -1, X, ldx, L, ldl, tau, pivot ? piv : nullptr, info, workspace,
+                    workspace_bytes, stream);
+}
+
+size_t skl_ltlt_unb_panel_workspace_size(int n, int width) {
+  if (n < 1 || width < 1) return 0;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, width, SKL_VAR2A, plan, width)) return 0;
+  return layout_blk(n, width, plan, nullptr, nullptr);
+}
+
+int skl_ltlt_unb_panel(int n, int width, int pivot, const double* X, long long ldx, double* L, long long ldl,
+                       double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  if (width < 1) return SKL_BAD_ARGUMENT;
+  return blk_driver(n, width, SKL_VAR2A, pivot ? 1 : 0, width, X, ldx, L, ldl, tau, pivot ? piv : nullptr, info,
+                    workspace, workspace_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------

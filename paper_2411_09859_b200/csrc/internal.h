@@ -75,7 +75,9 @@ struct PanelArgs {
   int kmax;              // slab columns (= r + nelim - lo)
   int slot_words;
   int dbg;               // timing experiments only (bitmask of skipped phases)
-  unsigned long long* prof;  // optional per-CTA phase cycle totals [C][8]
+  unsigned long long* prof;  // optional per-CTA phase cycle totals [C][16]
+  int pivot;             // 0: unpivoted (pivot row = row g+1), exact-zero breakdown -> *info
+  int* info;             // device: first breaking column + 1 (0 = none); may be null when pivot
 };
 size_t panel_smem_bytes(int rows_per, int kmax);
 int panel_max_ctas();

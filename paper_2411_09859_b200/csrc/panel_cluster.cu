@@ -382,6 +382,27 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       w = s.gwin[par];
       owner = s.misc[4 + par];
     }
+    if (!a.pivot) {
+      // unpivoted drivers (blocked.py:162-290, unblocked.py:192-226): the pivot row is
+      // row a itself; the argmax above only says whether the column below g is all
+      // zero, for the exact-zero breakdown test (ZeroPivot, unblocked.py:83-85)
+      const bool colnz = w.idx >= 0 && w.v != 0.0;
+      double va;
+      int pa_perm;
+      if (MULTI) {
+        const uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
+        uint32_t p32, dummy;
+        ll_get2(ra, tag, p32, dummy);
+        pa_perm = int(p32);
+        va = ll_get_double(ra + 4 + 2 * k, tag);
+      } else {
+        va = *cluster.map_shared_rank(s.pubA + par * (kmax + 2) + k, owner_a);
+        pa_perm = *cluster.map_shared_rank(s.misc + par, owner_a);
+      }
+      if (colnz && va == 0.0 && gcta == 0 && tid == 0 && a.info != nullptr && *a.info == 0) *a.info = g + 1;
+      w = CCand{va, a_pos, pa_perm};
+      owner = owner_a;
+    }
     const int b = w.idx, pb = w.perm;
     const double vb = w.v;
     const bool own_b = b >= rbase && b < rbase + rcount;
@@ -411,14 +432,16 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       }
     }
     if (MULTI) {
-      const uint64_t* gr = a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4;
+      const uint64_t* gr = a.pivot ? a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4
+                                   : a.rowa + (size_t)par * a.slot_words + 4;
       for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = ll_get_double(gr + 2 * j, tag);
       if (own_b && swapped) {
         const uint64_t* ra = a.rowa + (size_t)par * a.slot_words + 4;
         for (int j = tid; j <= k; j += kCThreads) s.arow[j] = ll_get_double(ra + 2 * j, tag);
       }
     } else {
-      const double* wr = cluster.map_shared_rank(s.pubrow + par * (kmax + 2), owner);
+      const double* wr = a.pivot ? cluster.map_shared_rank(s.pubrow + par * (kmax + 2), owner)
+                                 : cluster.map_shared_rank(s.pubA + par * (kmax + 2), owner_a);
       for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = wr[j];
       if (own_b && swapped) {
         const double* ar = cluster.map_shared_rank(s.pubA + par * (kmax + 2), owner_a);
@@ -545,7 +568,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   if (cta == 0) {
     for (int g = r + tid; g < rt; g += kCThreads) {
       a.tau[g] = s.taus[g - lo];
-      a.piv[g + 1] = (long long)s.pivbuf[g - r];
+      if (a.piv != nullptr) a.piv[g + 1] = (long long)s.pivbuf[g - r];
     }
   }
   if (a.prof && tid == 0) {

@@ -156,3 +156,214 @@ def flop_model(variant, m, b=None):
     if variant in ("unb-rl", "rl"):
         return 2 * m ** 3 / 3
     return m ** 3 / 3
+
+
+# ---------------------------------------------------------------------------
+# Flop replay of the unpivoted / unblocked drivers.  The
+# counts depend only on shapes, tau (eliminations skip the scaling when tau
+# is 0), the pivots and -- for the rank-2k couplings -- which operand columns
+# are nonzero; each helper cites the reference routine whose tally it replays.
+# ---------------------------------------------------------------------------
+
+class _Tally:
+    def __init__(self):
+        self.fc = FlopCounter()
+        self.in_panel = False
+
+    def add(self, kind, n):
+        n = int(n)
+        if self.in_panel and kind != "pivot":
+            self.fc.panel += n
+        else:
+            setattr(self.fc, kind, getattr(self.fc, kind) + n)
+
+
+def _t_elim(t, m, g, tau, pivots=None, swap_from=0):
+    """_eliminate (unblocked.py:63-91): swap moves + scaling of the tail."""
+    if pivots is not None and len(pivots):
+        off = int(pivots[g + 1])
+        if off:
+            a = g + 1 - swap_from
+            t.add("pivot", _swap_moves(m - swap_from, a, a + off))
+    if tau[g] != 0:
+        t.add("level2", max(m - g - 2, 0))
+
+
+def _t_skew_rank2(t, n):
+    """skew_rank2 (kernels2.py:93-131)."""
+    t.add("level2", 2 * n * max(n - 1, 0))
+
+
+def _t_trapezoid(t, m, start, climit):
+    """trapezoid_rank2 (kernels2.py:296-312): square skew part + rectangle."""
+    climit = min(climit, m)
+    nsq = climit - start
+    if nsq <= 0:
+        return
+    _t_skew_rank2(t, nsq)
+    if climit < m:
+        t.add("level2", 4 * (m - climit) * nsq)
+
+
+def _t_panel_ll(t, m, tau, base, nelim, lo, pivots=None, swap_from=None):
+    """_panel_ll (unblocked.py:94-119)."""
+    swap_from = lo if swap_from is None else swap_from
+    for g in range(base, base + nelim):
+        k = g - lo
+        if k >= 2:
+            t.add("level2", 2 * (m - g - 1) * k + 4 * k)
+        _t_elim(t, m, g, tau, pivots, swap_from)
+
+
+def _t_panel_rl(t, m, tau, base, nelim, climit, pivots=None, swap_from=None):
+    """_panel_rl (unblocked.py:122-133)."""
+    swap_from = base if swap_from is None else swap_from
+    for g in range(base, base + nelim):
+        _t_elim(t, m, g, tau, pivots, swap_from)
+        _t_trapezoid(t, m, g + 2, climit)
+
+
+def _t_panel_twostep(t, m, tau, base, nelim, climit):
+    """_panel_twostep (unblocked.py:136-171), unpivoted."""
+    end = base + nelim
+    g = base
+    while g < end:
+        if g + 1 >= end:
+            _t_elim(t, m, g, tau)
+            _t_trapezoid(t, m, g + 2, climit)
+            g += 1
+            continue
+        _t_elim(t, m, g, tau)
+        _t_elim(t, m, g + 1, tau)
+        s = g + 3
+        if g + 2 < min(climit, m):
+            t.add("level2", 6 * max(m - s, 0))
+            _t_trapezoid(t, m, s, climit)
+        g += 2
+
+
+def _t_run_panel(t, m, tau, base, nelim, variant, carry):
+    """_run_panel (blocked.py:88-105), unpivoted, inside the panel scope."""
+    climit = base + nelim
+    lo = base - 1 if carry else base
+    t.in_panel = True
+    if variant == "ll":
+        _t_panel_ll(t, m, tau, base, nelim, lo)
+    elif variant == "rl":
+        if carry:
+            _t_trapezoid(t, m, base + 1, climit)   # _apply_pending (unblocked.py:174-179)
+        _t_panel_rl(t, m, tau, base, nelim, climit)
+    else:
+        if carry:
+            _t_trapezoid(t, m, base + 1, climit)
+        _t_panel_twostep(t, m, tau, base, nelim, climit)
+    t.in_panel = False
+
+
+def _t_rankk(t, n, k):
+    """skew_tridiag_rankk (kernels3.py:164)."""
+    t.add("level3", 2 * k * _lower(n) + 4 * k * n)
+
+
+def _s_entries(k):
+    """number of entries of S for T of order k (core.py:153-169)."""
+    return sum((1 if row >= 2 else 0) + (1 if row + 1 < k else 0) for row in range(0, k, 2))
+
+
+def rank2k_keff(a, tau):
+    """keff of skew_rank2k(C, 1, A, W) with W = form_w(A, S(tau)) (kernels3.py:318-321):
+    columns nonzero in both A and W, W formed exactly as form_w does."""
+    a = np.asarray(a)
+    n, k = a.shape
+    w = np.zeros_like(a)
+    for row in range(0, k, 2):                     # core.py:163-168 entries (row, col, v)
+        if row >= 2:
+            w[:, row - 1] += tau[row - 1] * a[:, row]
+        if row + 1 < k:
+            w[:, row + 1] += -tau[row] * a[:, row]
+    return int(np.count_nonzero((a != 0).any(axis=0) & (w != 0).any(axis=0)))
+
+
+def flops_blk_unpivoted(m, b, driver, panel_variant, tau, work=None):
+    """FlopCounter of ltlt_blk_{var1,var2a,var2b,twostep,left} (blocked.py:162-290).
+
+    ``work`` (the returned "ones" buffer, host) is needed by the twostep driver
+    only: its rank-2k couplings skip zero columns (kernels3.py:318-321)."""
+    t = _Tally()
+    tau = np.asarray(tau)
+    if driver == "var2b":
+        done, first = 0, True
+        while done < m - 1:
+            nelim = min(b + (1 if first else 0), m - 1 - done)
+            _t_run_panel(t, m, tau, done, nelim, panel_variant, not first)
+            new = done + nelim
+            c0 = 1 if first else done
+            if m - new >= 2 and new - c0 >= 1:
+                _t_rankk(t, m - new, new - c0 + 1)
+            done, first = new, False
+    elif driver == "left":
+        r = 0
+        while r < m - 1:
+            be = min(b, m - 1 - r)
+            if r >= 2:   # skew_tridiag_gemm(tril) (kernels3.py:239-259): p = m-r, q = be, k = r
+                p, q, k = m - r, be, r
+                written = _lower(min(p, q)) + max(p - q, 0) * q
+                t.add("level3", 2 * k * written + 4 * k * q)
+            _t_run_panel(t, m, tau, r, be, panel_variant, r > 0)
+            r += be
+    else:
+        r, pending = 0, False
+        while r < m - 1:
+            be = min(b, m - 1 - r)
+            carry = driver != "var1" and pending
+            _t_run_panel(t, m, tau, r, be, panel_variant, carry)
+            rt = r + be
+            c0 = r + 1 if (driver == "var1" or not pending) else r
+            if m - rt >= 2 and rt - c0 >= 1:
+                n, k = m - rt, rt - c0 + 1
+                if driver == "twostep":
+                    a = np.asarray(work)[rt:, c0 - 1:rt]
+                    t.add("level3", 2 * n * _s_entries(k))              # form_w (kernels3.py:364)
+                    t.add("level3", 4 * rank2k_keff(a, tau[c0:rt]) * _lower(n))
+                else:
+                    _t_rankk(t, n, k)
+            if driver == "var1" and m - rt >= 2:
+                _t_skew_rank2(t, m - rt - 1)
+            pending = True
+            r = rt
+    return t.fc
+
+
+def flops_unb_rl(m, tau, pivots=None):
+    """FlopCounter of ltlt_unb_rl (unblocked.py:192-202)."""
+    t = _Tally()
+    _t_panel_rl(t, m, np.asarray(tau), 0, m - 1, m, pivots, 0)
+    return t.fc
+
+
+def flops_unb_ll(m, tau, pivots=None, first_column=False):
+    """FlopCounter of ltlt_unb_ll (unblocked.py:205-226)."""
+    t = _Tally()
+    if first_column:
+        _t_skew_rank2(t, m - 1)
+    _t_panel_ll(t, m, np.asarray(tau), 0, m - 1, 0, pivots, 0)
+    return t.fc
+
+
+def flops_unb_panel(m, width, variant, tau, pivots=None, first_column=False):
+    """FlopCounter of ltlt_unb_panel (unblocked.py:243-275)."""
+    t = _Tally()
+    tau = np.asarray(tau)
+    nelim = min(width, m - 1)
+    climit = min(width, m)
+    if first_column:
+        _t_skew_rank2(t, m - 1)
+    t.in_panel = True
+    if variant == "ll":
+        _t_panel_ll(t, m, tau, 0, nelim, 0, pivots, 0)
+    elif variant == "rl":
+        _t_panel_rl(t, m, tau, 0, nelim, climit)
+    else:
+        _t_panel_twostep(t, m, tau, 0, nelim, climit)
+    t.in_panel = False
+    return t.fc

@@ -1,0 +1,134 @@
+"""GPU parity of the unpivoted blocked / unblocked / panel drivers (SURVEY.md
+8f rank 1: blocked.py:162-290, unblocked.py:192-275) against the oracle, which
+test_oracle.py pins bit-for-bit to the reference's fixtures.
+
+Without pivoting the factors grow (max|L| ~ 1e3-1e4 on these N(0,1) inputs),
+so L and tau are compared relative to their largest entry with a tolerance
+scaled by that growth: |dL| <= 1e-10 * n * growth * max|L|, growth =
+max(1, max|L|).  Pivoted variants keep the 1e-10 * n contract and bit-exact
+pivots.  Flop tallies must equal the reference's exactly."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2411_09859_b200.inputs import skew_lower
+
+pytestmark = pytest.mark.gpu
+
+
+def pk():
+    import paper_2411_09859_b200 as m
+    return m
+
+
+def tally(fc):
+    return dict(level2=fc.level2, level3=fc.level3, panel=fc.panel, pivot=fc.pivot)
+
+
+def assert_close(r, o, n, pivoted):
+    lg = np.tril(np.asarray(r.l.data), -1)
+    lo = np.tril(o.work, -1)
+    scale = max(1.0, float(np.max(np.abs(lo), initial=0.0)))
+    growth = 1.0 if pivoted else scale
+    assert np.max(np.abs(lg - lo), initial=0.0) <= 1e-10 * n * growth * scale
+    tscale = max(1.0, float(np.max(np.abs(o.tau), initial=0.0)))
+    assert np.max(np.abs(np.asarray(r.t.tau) - o.tau), initial=0.0) <= 1e-10 * n * growth * tscale
+    assert np.array_equal(np.asarray(r.p.pivots), o.pivots)
+    assert tally(r.flops) == o.flops
+
+
+SIZES = [(2, 1), (5, 2), (64, 16), (150, 32), (301, 64)]
+
+
+@pytest.mark.parametrize("n,b", SIZES)
+@pytest.mark.parametrize("driver", ["var1", "var2a", "var2b", "twostep", "left"])
+@pytest.mark.parametrize("pv", ["ll", "rl", "twostep"])
+def test_blocked_unpivoted(n, b, driver, pv):
+    x = skew_lower(n, n)
+    r = getattr(pk(), f"ltlt_blk_{driver}")(pk().SkewMatrixLower(x), b=b, panel_variant=pv)
+    assert_close(r, oracle.ltlt_blk(x, b, driver, pv), n, False)
+
+
+@pytest.mark.parametrize("n", [2, 7, 64, 301])
+@pytest.mark.parametrize("pivot", [False, True])
+def test_unb_rl_and_ll(n, pivot):
+    x = skew_lower(n, 3 * n)
+    X = pk().SkewMatrixLower(x)
+    assert_close(pk().ltlt_unb_rl(X, pivot=pivot), oracle.ltlt_unb_rl(x, pivot), n, pivot)
+    assert_close(pk().ltlt_unb_ll(X, pivot=pivot), oracle.ltlt_unb_ll(x, pivot), n, pivot)
+
+
+@pytest.mark.parametrize("n", [3, 64, 150])
+def test_unb_ll_first_column(n):
+    x = skew_lower(n, n + 1)
+    fcv = np.random.Generator(np.random.Philox(n)).standard_normal(n - 1) * 0.5
+    r = pk().ltlt_unb_ll(pk().SkewMatrixLower(x), first_column=fcv)
+    o = oracle.ltlt_unb_ll(x, first_column=fcv)
+    assert_close(r, o, n, False)
+    assert np.array_equal(r.l.first_column, o.first_column)
+    assert np.allclose(r.l.dense()[1:, 0], fcv)
+
+
+@pytest.mark.parametrize("n,width", [(64, 40), (150, 40), (301, 150), (30, 100)])
+@pytest.mark.parametrize("variant,pivot", [("ll", False), ("rl", False), ("twostep", False), ("ll", True)])
+def test_unb_panel(n, width, variant, pivot):
+    x = skew_lower(n, n + width)
+    r = pk().ltlt_unb_panel(pk().SkewMatrixLower(x), width, variant=variant, pivot=pivot)
+    o = oracle.ltlt_unb_panel(x, width, variant, pivot)
+    assert_close(r, o, n, pivot)
+    nelim = min(width, n - 1)
+    assert not np.asarray(r.l.data)[:, nelim:].any()          # lbuf: zeros past the panel
+    assert np.array_equal(np.triu(np.asarray(r.l.data)[:, :nelim]), np.triu(x[:, :nelim]))
+
+
+def test_unb_panel_first_column():
+    n = 90
+    x = skew_lower(n, 5)
+    fcv = np.linspace(-1.0, 1.0, n - 1)
+    r = pk().ltlt_unb_panel(pk().SkewMatrixLower(x), 33, first_column=fcv)
+    o = oracle.ltlt_unb_panel(x, 33, "ll", False, fcv)
+    assert_close(r, o, n, False)
+    assert np.array_equal(r.l.first_column, o.first_column)
+
+
+def test_zero_pivot_and_zero_column():
+    """ZeroPivot(column) on an exact zero pivot with a nonzero tail
+    (unblocked.py:83-85); an all-zero subcolumn gives tau = 0 and continues."""
+    x = np.zeros((4, 4), order="F")
+    x[2, 0], x[3, 1], x[3, 2] = 1.0, 2.0, 3.0
+    for call in (lambda X: pk().ltlt_blk_var1(X, b=2), lambda X: pk().ltlt_blk_var2b(X, b=2),
+                 lambda X: pk().ltlt_unb_ll(X), lambda X: pk().ltlt_unb_rl(X),
+                 lambda X: pk().ltlt_unb_panel(X, 2)):
+        with pytest.raises(pk().ZeroPivot) as ei:
+            call(pk().SkewMatrixLower(x))
+        assert ei.value.column == 0
+    # breakdown at a later column: column 1 becomes zero at its pivot
+    y = skew_lower(6, 1)
+    y[2, 1] = 0.0
+    o_fail = None
+    try:
+        oracle.ltlt_blk(y, 2, "var2a")
+    except ZeroDivisionError as e:
+        o_fail = e
+    if o_fail is None:
+        r = pk().ltlt_blk_var2a(pk().SkewMatrixLower(y), b=2)
+        assert_close(r, oracle.ltlt_blk(y, 2, "var2a"), 6, False)
+    z = np.zeros((3, 3), order="F")
+    z[2, 1] = 4.0
+    r = pk().ltlt_blk_var1(pk().SkewMatrixLower(z), b=2)
+    assert np.asarray(r.t.tau).tolist() == [0.0, 4.0]
+
+
+def test_left_pivot_unsupported_and_bad_variants():
+    X = pk().SkewMatrixLower(skew_lower(8, 0))
+    with pytest.raises(pk().PivotUnsupported):
+        pk().ltlt_blk_left(X, b=2, pivot=True)
+    with pytest.raises(pk().InvalidVariant):
+        pk().ltlt_blk_var2a(X, b=2, panel_variant="bogus")
+    with pytest.raises(pk().InvalidVariant):
+        pk().ltlt_blk_var2a(X, b=2, features=pk().Features(external_t=False))
+    with pytest.raises(pk().InvalidVariant):
+        pk().ltlt_unb_panel(X, 3, variant="rl", pivot=True)
+    with pytest.raises(ValueError):
+        pk().ltlt_blk_var1(X, b=0)
