@@ -38,6 +38,38 @@ __device__ __forceinline__ void ll_get2(const uint64_t* p, uint32_t flag, uint32
   d1 = uint32_t(w1);
 }
 
+// three flagged pairs (a 6-word record) polled together: one L2 round trip per
+// attempt instead of three dependent ones
+__device__ __forceinline__ void ll_get6(const uint64_t* p, uint32_t flag, uint32_t& d0, uint32_t& d1, uint32_t& d2,
+                                        uint32_t& d3, uint32_t& d4, uint32_t& d5) {
+  uint64_t w0, w1, w2, w3, w4, w5;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(p + 2) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w4), "=l"(w5) : "l"(p + 4) : "memory");
+  } while (uint32_t(w0 >> 32) != flag || uint32_t(w1 >> 32) != flag || uint32_t(w2 >> 32) != flag ||
+           uint32_t(w3 >> 32) != flag || uint32_t(w4 >> 32) != flag || uint32_t(w5 >> 32) != flag);
+  d0 = uint32_t(w0);
+  d1 = uint32_t(w1);
+  d2 = uint32_t(w2);
+  d3 = uint32_t(w3);
+  d4 = uint32_t(w4);
+  d5 = uint32_t(w5);
+}
+
+// two flagged doubles from independent places, polled together
+__device__ __forceinline__ void ll_get_double2(const uint64_t* p, const uint64_t* q, uint32_t flag, double& x,
+                                               double& y) {
+  uint64_t w0, w1, w2, w3;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(q) : "memory");
+  } while (uint32_t(w0 >> 32) != flag || uint32_t(w1 >> 32) != flag || uint32_t(w2 >> 32) != flag ||
+           uint32_t(w3 >> 32) != flag);
+  x = __longlong_as_double((long long)((uint64_t(uint32_t(w1)) << 32) | uint32_t(w0)));
+  y = __longlong_as_double((long long)((uint64_t(uint32_t(w3)) << 32) | uint32_t(w2)));
+}
+
 __device__ __forceinline__ double ll_get_double(const uint64_t* p, uint32_t flag) {
   uint32_t lo, hi;
   ll_get2(p, flag, lo, hi);

@@ -62,6 +62,12 @@ __device__ __forceinline__ void cwarp_argmax(CCand& c, int& owner) {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 
 // Exact warp argmax of |v| with ties to the lowest index, using three
 // redux.sync reductions on the bit pattern of |v| (monotone for v >= 0)
@@ -295,6 +301,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     __syncthreads();
 
     // ---- (2) CTA candidate -> every CTA of the cluster; publish rows ------------
+    int lc_pub = -1;  // local row of this CTA's candidate (warp 0)
     if (warp == 0) {
       const bool ok = lane < kCWarps && s.wcand[lane].idx >= 0;
       const CCand mine = lane < kCWarps ? s.wcand[lane] : CCand{0.0, -1, 0};
@@ -304,31 +311,39 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       if (id >= 0) {
         c = s.wcand[__ffs(bal) - 1];
         c.perm = s.perm[c.idx - rbase];
-        const int lc = c.idx - rbase;
-        double* pr = s.pubrow + par * (kmax + 2);
-        if (MULTI) {
-          uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
-          for (int j = lane; j <= k; j += 32) ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc], tag);
-        } else {
-          for (int j = lane; j <= k; j += 32) pr[j] = s.slab[(size_t)j * Rs + lc];
+        lc_pub = c.idx - rbase;
+        if (!MULTI) {
+          double* pr = s.pubrow + par * (kmax + 2);
+          for (int j = lane; j <= k; j += 32) pr[j] = s.slab[(size_t)j * Rs + lc_pub];
         }
       }
       __syncwarp();
       if (lane < C) *cluster.map_shared_rank(s.cand + par * kClusterMax + crank, lane) = c;
-    } else if (warp == 1 && own_a) {
+    } else if (!MULTI && warp == 1 && own_a) {
       const int la = a_pos - rbase;
-      if (MULTI) {
+      double* pa = s.pubA + par * (kmax + 2);
+      for (int j = lane; j <= k; j += 32) pa[j] = s.slab[(size_t)j * Rs + la];
+      if (lane == 0) s.misc[par] = s.perm[la];
+    }
+    CMARK(1);
+    if (MULTI) {
+      // the global LL publications (candidate row, row a) carry their own flags and
+      // need no ordering: issue them between the barrier's arrive and wait so the
+      // release does not wait for their L2 round trip
+      cluster_arrive_release();
+      if (warp == 0 && lc_pub >= 0) {
+        uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
+        for (int j = lane; j <= k; j += 32) ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc_pub], tag);
+      } else if (warp == 1 && own_a) {
+        const int la = a_pos - rbase;
         uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
         for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
         if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
-      } else {
-        double* pa = s.pubA + par * (kmax + 2);
-        for (int j = lane; j <= k; j += 32) pa[j] = s.slab[(size_t)j * Rs + la];
-        if (lane == 0) s.misc[par] = s.perm[la];
       }
+      cluster_wait_acquire();
+    } else {
+      cluster_barrier();
     }
-    CMARK(1);
-    cluster_barrier();
     CMARK(2);
 
     // ---- (3) winner, next-column gather, winner row / row a via DSMEM ---------
@@ -357,9 +372,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         if (lane < Q) {
           const uint64_t* rq = a.recs + ((size_t)par * Q + lane) * 6;
           uint32_t lo32, hi32, ci, cp, ow, dummy;
-          ll_get2(rq, tag, lo32, hi32);
-          ll_get2(rq + 2, tag, ci, cp);
-          ll_get2(rq + 4, tag, ow, dummy);
+          ll_get6(rq, tag, lo32, hi32, ci, cp, ow, dummy);
           o.v = __longlong_as_double((long long)((uint64_t(hi32) << 32) | lo32));
           o.idx = int(ci);
           o.perm = int(cp);
@@ -409,23 +422,18 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     const bool swapped = b != a_pos;
     const bool more = (g + 1 < rt) || a.want_y;
     int perm_a = 0;
-    if (own_b && swapped) {
-      if (MULTI) {
-        uint32_t pa32, dummy;
-        ll_get2(a.rowa + (size_t)par * a.slot_words, tag, pa32, dummy);
-        perm_a = int(pa32);
-      } else {
-        perm_a = *cluster.map_shared_rank(s.misc + par, owner_a);
-      }
-    }
+    const bool need_a = own_b && swapped;  // row b's owner receives row a
+    const int lb_thread = (b - rbase) & (kCThreads - 1);
+    // gathers of the next column for every row but b (row b's physical index
+    // perm_a arrives with row a; its gather is issued once that is known)
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int li = tid + u * kCThreads;
       const int pos = rbase + li;
       cnext[u] = 0.0;
       cneg[u] = false;
-      if (more && li < rcount && pos > a_pos) {
-        const int ph = (swapped && pos == b) ? perm_a : s.perm[li];
+      if (more && li < rcount && pos > a_pos && !(need_a && pos == b)) {
+        const int ph = s.perm[li];
         // X(ph, pb) in skew-lower storage; the sign is applied when consumed
         cneg[u] = ph < pb;
         cnext[u] = cneg[u] ? W[(long long)ph * ld + pb] : W[(long long)pb * ld + ph];
@@ -434,19 +442,41 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     if (MULTI) {
       const uint64_t* gr = a.pivot ? a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4
                                    : a.rowa + (size_t)par * a.slot_words + 4;
-      for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = ll_get_double(gr + 2 * j, tag);
-      if (own_b && swapped) {
-        const uint64_t* ra = a.rowa + (size_t)par * a.slot_words + 4;
-        for (int j = tid; j <= k; j += kCThreads) s.arow[j] = ll_get_double(ra + 2 * j, tag);
+      const uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
+      if (need_a) {
+        // pivot row, row a and row a's header polled together (one round trip)
+        for (int j = tid; j <= k; j += kCThreads) ll_get_double2(gr + 2 * j, ra + 4 + 2 * j, tag, s.wrow[j], s.arow[j]);
+        if (tid == lb_thread) {
+          uint32_t pa32, dummy;
+          ll_get2(ra, tag, pa32, dummy);
+          perm_a = int(pa32);
+        }
+      } else {
+        for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = ll_get_double(gr + 2 * j, tag);
       }
     } else {
       const double* wr = a.pivot ? cluster.map_shared_rank(s.pubrow + par * (kmax + 2), owner)
                                  : cluster.map_shared_rank(s.pubA + par * (kmax + 2), owner_a);
-      for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = wr[j];
-      if (own_b && swapped) {
+      if (need_a) {
         const double* ar = cluster.map_shared_rank(s.pubA + par * (kmax + 2), owner_a);
-        for (int j = tid; j <= k; j += kCThreads) s.arow[j] = ar[j];
+        if (tid == lb_thread) perm_a = *cluster.map_shared_rank(s.misc + par, owner_a);
+        for (int j = tid; j <= k; j += kCThreads) {
+          const double wv = wr[j], av = ar[j];
+          s.wrow[j] = wv;
+          s.arow[j] = av;
+        }
+      } else {
+        for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = wr[j];
       }
+    }
+    if (need_a && tid == lb_thread) {
+      const int u = (b - rbase) >> 8;  // kCThreads == 256
+#pragma unroll
+      for (int uu = 0; uu < 2; ++uu)
+        if (uu == u && more) {
+          cneg[uu] = perm_a < pb;
+          cnext[uu] = cneg[uu] ? W[(long long)perm_a * ld + pb] : W[(long long)pb * ld + perm_a];
+        }
     }
     __syncthreads();
     CMARK(3);
