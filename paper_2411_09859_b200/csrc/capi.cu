@@ -133,8 +133,13 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
       while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo) > smem_limit()) --w;
       static int min_w = env_int("SKL_MIN_CLUSTER_W", 64);
+      static int ll_single = env_int("SKL_LL_SINGLE", 1);
       if (w >= 1 && w >= std::min(want, min_w)) {
-        p = PanelPlan{r, w, lo, C, Rc, r + w - lo, 1, C};
+        // default (SKL_LL_SINGLE=1): the one cluster runs the multi-cluster kernel with
+        // Q = 1 -- st.async candidate all-to-all + flagged pivot rows through L2, no
+        // cluster barrier per step (2-3 % faster than the DSMEM-pull variant, which
+        // SKL_LL_SINGLE=0 keeps)
+        p = ll_single ? PanelPlan{r, w, lo, C, Rc, r + w - lo, 2, C} : PanelPlan{r, w, lo, C, Rc, r + w - lo, 1, C};
         return true;
       }
     }

@@ -62,6 +62,18 @@ __device__ __forceinline__ void cwarp_argmax(CCand& c, int& owner) {
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// 16-byte candidate -> the same smem slot in CTA `rank`, completing 16 bytes of
+// transaction on that CTA's mbarrier (same offset as `bar`)
+__device__ __forceinline__ void st_async_cand(CCand* slot_local, uint64_t* bar_local, uint32_t rank, const CCand& c) {
+  uint32_t rdst, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(slot_local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(bar_local)), "r"(rank));
+  const unsigned long long vb = (unsigned long long)__double_as_longlong(c.v);
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(rdst),
+               "r"(uint32_t(vb)), "r"(uint32_t(vb >> 32)), "r"(uint32_t(c.idx)), "r"(uint32_t(c.perm)), "r"(rbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void cluster_arrive_release() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -101,6 +113,7 @@ struct CSmem {
   int* misc;       // [0..1] pubA perm per parity, [4..5] global winner owner (MULTI)
   int* pivbuf;     // [nelim] pivot offsets of this panel (flushed at the end)
   CCand* gwin;     // [2] global winner (MULTI)
+  uint64_t* xbar;  // MULTI: [0..1] candidate all-to-all, [2..3] global-winner delivery (st.async)
 };
 
 __host__ __device__ inline int cslab_stride(int rows_per) { return rows_per | 1; }
@@ -147,6 +160,8 @@ __host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsign
   if (s) s->pivbuf = (int*)p;
   p = take(sizeof(CCand) * 2);
   if (s) s->gwin = (CCand*)p;
+  p = take(sizeof(uint64_t) * 4);
+  if (s) s->xbar = (uint64_t*)p;
   return off;
 }
 
@@ -222,6 +237,10 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 
   CSmem s;
   csmem_layout(R, kmax, &s, smem_raw);
+  if (MULTI && tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);  // one local arrival (expect_tx) per phase
+    fence_mbar_init();  // made visible to the cluster by the cluster barrier below
+  }
 
   for (int li = tid; li < rcount; li += kCThreads) {
     s.perm[li] = rbase + li;
@@ -276,6 +295,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     const bool own_a = owner_a == cta;
     const uint32_t tag = a.tag0 + uint32_t(g - r);
 
+    if (MULTI && tid == 0) {
+      // this step's deliveries: C candidates (16 B each) and the global winner (16 B)
+      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C) * sizeof(CCand));
+      if (Q > 1) mbar_arrive_expect_tx(&s.xbar[2 + par], sizeof(CCand));
+    }
+
     // ---- (1) v = c - A z; per-warp argmax -----------------------------------
     double vbest = 0.0;
     int ibest = -1;
@@ -318,7 +343,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         }
       }
       __syncwarp();
-      if (lane < C) *cluster.map_shared_rank(s.cand + par * kClusterMax + crank, lane) = c;
+      if (MULTI) {
+        // candidate -> slot crank of every cluster CTA, delivered with its mbarrier
+        if (lane < C) st_async_cand(s.cand + par * kClusterMax + crank, &s.xbar[par], lane, c);
+      } else if (lane < C) {
+        *cluster.map_shared_rank(s.cand + par * kClusterMax + crank, lane) = c;
+      }
     } else if (!MULTI && warp == 1 && own_a) {
       const int la = a_pos - rbase;
       double* pa = s.pubA + par * (kmax + 2);
@@ -328,9 +358,8 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     CMARK(1);
     if (MULTI) {
       // the global LL publications (candidate row, row a) carry their own flags and
-      // need no ordering: issue them between the barrier's arrive and wait so the
-      // release does not wait for their L2 round trip
-      cluster_arrive_release();
+      // need no ordering; the candidates arrive by st.async on xbar[par] (no
+      // cluster barrier: nothing else is read across CTAs in this mode)
       if (warp == 0 && lc_pub >= 0) {
         uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
         for (int j = lane; j <= k; j += 32) ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc_pub], tag);
@@ -340,7 +369,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
         if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
       }
-      cluster_wait_acquire();
+      mbar_wait_acq_cluster(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
     } else {
       cluster_barrier();
     }
@@ -357,7 +386,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       w = s.cand[par * kClusterMax + owner];
       owner += qid * C;  // global CTA id of the cluster's best
     }
-    if (MULTI) {
+    if (MULTI && Q > 1) {
       if (crank == 0 && warp == 0) {
         // leader: publish the cluster's best, gather every cluster's best (one lane each)
         uint64_t* rec = a.recs + ((size_t)par * Q + qid) * 6;
@@ -385,15 +414,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         gw.v = __shfl_sync(0xffffffffu, o.v, wl);
         gw.idx = __shfl_sync(0xffffffffu, o.idx, wl);
         gw.perm = __shfl_sync(0xffffffffu, o.perm, wl);
-        const int gow = __shfl_sync(0xffffffffu, oo, wl);
-        if (lane < C) {
-          *cluster.map_shared_rank(s.gwin + par, lane) = gw;
-          *cluster.map_shared_rank(s.misc + 4 + par, lane) = gow;
-        }
+        (void)oo;
+        if (lane < C) st_async_cand(s.gwin + par, &s.xbar[2 + par], lane, gw);
       }
-      cluster_barrier();
+      mbar_wait_acq_cluster(&s.xbar[2 + par], (uint32_t(g - r) >> 1) & 1u);
       w = s.gwin[par];
-      owner = s.misc[4 + par];
+      owner = w.idx >= 0 ? (w.idx - row0) / R : 0;  // rows are dealt out contiguously
     }
     if (!a.pivot) {
       // unpivoted drivers (blocked.py:162-290, unblocked.py:192-226): the pivot row is
