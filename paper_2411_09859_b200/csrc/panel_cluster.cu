@@ -847,7 +847,9 @@ cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t strea
   attrs[1].id = cudaLaunchAttributeCooperative;
   attrs[1].val.cooperative = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = 2;
+  // co-residency only matters across clusters; one cluster is co-resident by
+  // construction (and a plain cluster launch stays replayable under ncu)
+  cfg.numAttrs = a.nblocks > csize ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel<true>, a);
   if (e != cudaSuccess) return e;
   return launch_panel_finish(a, stream);
