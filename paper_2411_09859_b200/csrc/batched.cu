@@ -151,6 +151,27 @@ __device__ void bsym_swap(const BCtx<T>& c, int a, int b) {
   if (tid == 0) pa[b] = -pa[b];
 }
 
+#ifdef SKL_BATCHED_PROF
+__device__ unsigned long long g_bprof[8];
+}  // namespace
+}  // namespace skl
+extern "C" int skl_debug_read_bprof(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, skl::g_bprof, sizeof(unsigned long long) * 8);
+}
+namespace skl {
+namespace {
+#define BMARK(i)                                                         \
+  do {                                                                   \
+    long long _t = clock64();                                            \
+    if (threadIdx.x == 0 && blockIdx.x == 0) bpt[i] += _t - bprev;       \
+    bprev = _t;                                                          \
+  } while (0)
+#else
+#define BMARK(i) \
+  do {           \
+  } while (0)
+#endif
+
 template <typename T>
 __global__ void __launch_bounds__(kBThreads, 1)
 batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx, long long strideX, T* __restrict__ L,
@@ -197,11 +218,17 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
     double logabs = 0.0, sgn = 1.0;
     const int end = n - 1;
     int g = 0;
+#ifdef SKL_BATCHED_PROF
+    long long bpt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long bprev = clock64();
+#endif
     while (g < end) {
       // ---- eliminate(g): argmax, interchange + scale in one pass -------------
+      BMARK(7);
       int b = col_argmax(c, g, redv, redi);
       const T t0 = c.col(g)[b];  // becomes X[g+1, g] after the interchange
       __syncthreads();            // every warp has read the partials and tau
+      BMARK(0);
       swap_and_eliminate(c, g, b, t0);
       if (tid == 0) {
         pm[g + 1] = b - (g + 1);
@@ -213,6 +240,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         }
       }
       __syncthreads();
+      BMARK(1);
       if (tid == 0) c.col(g)[g + 1] = T(1);
       if (g + 1 >= end) {
         __syncthreads();
@@ -223,6 +251,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
       b = col_argmax(c, g + 1, redv, redi);
       const T t1 = c.col(g + 1)[b];
       __syncthreads();
+      BMARK(2);
       swap_and_eliminate(c, g + 1, b, t1);
       if (tid == 0) {
         pm[g + 2] = b - (g + 2);
@@ -230,6 +259,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         tm[g + 1] = t1;
       }
       __syncthreads();
+      BMARK(3);
       // ---- fold the first coupling into column g+2, rank-2 vectors ----------
       const int s0 = g + 3;
       T* xg = c.col(g);
@@ -245,6 +275,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         vec[n + i] = l2;
       }
       __syncthreads();
+      BMARK(4);
       if (tid == 0) x1[g + 2] = T(1);
       // ---- X[s:, s:] -= wv l2^T - l2 wv^T -------------------------------------
       if (s0 < n) {
@@ -278,8 +309,13 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         }
       }
       __syncthreads();
+      BMARK(5);
       g += 2;
     }
+#ifdef SKL_BATCHED_PROF
+    if (tid == 0 && blockIdx.x == 0)
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_bprof[i], (unsigned long long)bpt[i]);
+#endif
     if (tid == 0) {
       if (n % 2 == 1) {
         if (pf_sign) pf_sign[m] = 0.0;
