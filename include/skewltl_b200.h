@@ -117,6 +117,17 @@ int skl_ltlt_unb_panel(int n, int width, int pivot, const double* X, long long l
                        double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* solve (apps.py:76-100): X y = b from a pivoted factorization (L "ones"
+ *   buffer, tau, piv as written by skl_ltlt_blk_piv).  B (n x nrhs, device,
+ *   column-major) is overwritten by y.  A numerically singular T (a pivot at or
+ *   below tol_scale * eps * max|tau|, apps.py:47-65; every odd n) stores the
+ *   row + 1 in the device int *info (0 = success) -- SingularT on the host --
+ *   and B is then meaningless.                                                */
+size_t skl_ltlt_solve_workspace_size(int n, int nrhs);
+int skl_ltlt_solve(int n, int nrhs, const double* L, long long ldl, const double* tau, const long long* piv,
+                   double* B, long long ldb, double tol_scale, int* info, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
 /* Same factorization from HOST buffers (the drop-in call with H2D/D2H inside;
  * X_host/L_host column-major, pinned for asynchronous copies).  Only the
  * lower part travels: column blocks [j0, j0+128) move rows [j0, n), i.e. the

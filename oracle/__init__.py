@@ -30,6 +30,8 @@ from .ltlt import (  # noqa: F401
     ltlt_unb_rl,
     ltlt_unb_twostep,
     skew_tridiag_gemm,
+    solve,
+    tridiag_solve,
     l_dense,
     pfaffian,
     pfaffian_slog,

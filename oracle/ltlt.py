@@ -754,6 +754,70 @@ def pfaffian(x, b=None):
     return val
 
 
+def tridiag_solve(tau, rhs, tol_scale=10.0):
+    """T y = rhs by Gaussian elimination with partial pivoting, one extra
+    superdiagonal of fill (apps.py:33-73).  Raises ZeroDivisionError where the
+    reference raises SingularT (pivot at or below tol_scale eps max|tau|)."""
+    m = len(tau) + 1
+    x = np.array(rhs, dtype=float)
+    if x.shape[0] != m:
+        raise ValueError("dimension mismatch")
+    d = np.zeros(m)
+    e = np.zeros(m)
+    f2 = np.zeros(m)
+    sub = np.array(tau, dtype=float)
+    if m > 1:
+        e[:m - 1] = -sub
+    big = float(np.max(np.abs(sub))) if m > 1 else 0.0
+    thresh = tol_scale * np.finfo(float).eps * big
+    for k in range(m - 1):
+        if abs(sub[k]) > abs(d[k]):
+            d[k], sub[k] = sub[k], d[k]
+            e[k], d[k + 1] = d[k + 1], e[k]
+            if k + 2 < m:
+                f2[k], e[k + 1] = e[k + 1], f2[k]
+            x[[k, k + 1]] = x[[k + 1, k]]
+        if abs(d[k]) <= thresh:
+            raise ZeroDivisionError(f"tridiagonal pivot at row {k}")
+        mult = sub[k] / d[k]
+        d[k + 1] -= mult * e[k]
+        if k + 2 < m:
+            e[k + 1] -= mult * f2[k]
+        x[k + 1] -= mult * x[k]
+    if abs(d[m - 1]) <= thresh:
+        raise ZeroDivisionError(f"tridiagonal pivot at row {m - 1}")
+    x[m - 1] /= d[m - 1]
+    if m > 1:
+        x[m - 2] = (x[m - 2] - e[m - 2] * x[m - 1]) / d[m - 2]
+    for k in range(m - 3, -1, -1):
+        x[k] = (x[k] - e[k] * x[k + 1] - f2[k] * x[k + 2]) / d[k]
+    return x
+
+
+def solve(x, b, block=None, tol_scale=10.0):
+    """X y = b through the pivoted factorization (apps.py:76-100): permute,
+    unit-lower solve, pivoted tridiagonal solve, transposed unit-lower solve,
+    permute back.  Multiple right-hand sides as columns."""
+    from scipy.linalg import solve_triangular
+    x = np.asarray(x)
+    m = x.shape[0]
+    b = np.asarray(b, dtype=float)
+    one_d = b.ndim == 1
+    rhs = b.reshape(m, -1) if one_d else b
+    if rhs.shape[0] != m:
+        raise ValueError("dimension mismatch")
+    res = ltlt_blk_piv(x, b=block or min(DEFAULT_BLOCK, m))
+    perm = compose_permutation(res.pivots)
+    z = rhs[perm]
+    ld = l_dense(res.work)
+    z = solve_triangular(ld, z, lower=True, unit_diagonal=True)
+    z = tridiag_solve(res.tau, z, tol_scale=tol_scale)
+    z = solve_triangular(ld, z, trans="T", lower=True, unit_diagonal=True)
+    out = np.empty_like(z)
+    out[perm] = z
+    return out.ravel() if one_d else out
+
+
 def pfaffian_slog(tau, pivots, m):
     """(sign, log|Pf|) from tau and the pivot parity; overflow-free form of
     apps.py:26-30.  Pf = sign(P) prod_{i even} (-tau_i)."""

@@ -13,5 +13,6 @@ from .blocked import (DEFAULT_BLOCK, FactorizationResult, Features, ltlt_blk_dev
                       ltlt_blk_left, ltlt_blk_piv, ltlt_blk_piv_device, ltlt_blk_piv_host, ltlt_blk_twostep,
                       ltlt_blk_var1, ltlt_blk_var2a, ltlt_blk_var2b)
 from .unblocked import ltlt_unb_ll, ltlt_unb_panel, ltlt_unb_rl, ltlt_unb_twostep  # noqa: F401
+from .apps import pfaffian, solve  # noqa: F401
 
 __version__ = "0.1.0"

@@ -40,6 +40,8 @@ SIGNATURES = {
     "skl_ltlt_blk": (_i, [_i, _i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
     "skl_ltlt_unb_panel_workspace_size": (_sz, [_i, _i]),
     "skl_ltlt_unb_panel": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
+    "skl_ltlt_solve_workspace_size": (_sz, [_i, _i]),
+    "skl_ltlt_solve": (_i, [_i, _i, _p, _ll, _p, _p, _p, _ll, _d, _p, _p, _sz, _p]),
     "skl_ltlt_blk_piv_host_workspace_size": (_sz, [_i, _i, _i]),
     "skl_ltlt_blk_piv_host": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _sz, _p]),
     "skl_ltlt_unb_twostep_workspace_size": (_sz, [_i]),

@@ -5,7 +5,8 @@ Pf = sign(P) prod_{i even} (-tau_i), Pf([[0, a], [-a, 0]]) = a, odd m -> 0,
 m == 0 -> 1.  Like the reference it can overflow to inf for large m, so
 ``pfaffian_slog`` returns the overflow-free (sign, log|Pf|).
 ``pfaffian_batched`` is the batched B200 path (config 4): many independent
-matrices in one launch, (sign, log|Pf|) per matrix.
+matrices in one launch, (sign, log|Pf|) per matrix.  ``solve`` (apps.py:76-100)
+runs the permuted triangular / tridiagonal solves on the device.
 """
 
 from __future__ import annotations
@@ -46,6 +47,66 @@ def pfaffian(x: SkewMatrixLower, b=None):
     for i in range(0, m - 1, 2):
         val = val * (-float(tau[i]))
     return val
+
+
+def solve(x: SkewMatrixLower, b, block=None, tol_scale=10.0):
+    """Solve X y = b through the pivoted factorization (apps.py:76-100):
+    permute, unit-lower solve, pivoted skew-tridiagonal solve, transposed
+    unit-lower solve, permute back -- all on the device (``skl_ltlt_solve``
+    after ``skl_ltlt_blk_piv``).  ``b`` may hold several right-hand sides as
+    columns.  Raises SingularT for a numerically singular X (every odd m)."""
+    from . import _capi
+    from . import device as dv
+    from .blocked import ltlt_blk_piv_device
+    from .core import SingularT
+
+    if not isinstance(x, SkewMatrixLower):
+        x = SkewMatrixLower(x)
+    m = x.m
+    t = dv.require_cuda()
+    on_device = dv.is_colmajor_cuda(x.data)
+    bd_in = b if dv._is_cuda_tensor(b) else None
+    bh = None if bd_in is not None else np.asarray(b, dtype=float)
+    one_d = (bd_in.dim() if bd_in is not None else bh.ndim) == 1
+    if bd_in is not None:
+        rhs = bd_in.reshape(m, -1) if one_d else bd_in
+        if rhs.shape[0] != m:
+            raise ValueError("dimension mismatch")
+        bdev = dv.empty_colmajor(m, rhs.shape[1], t.float64)
+        bdev.copy_(rhs)
+    else:
+        rhs = bh.reshape(m, -1) if one_d else bh
+        if rhs.shape[0] != m:
+            raise ValueError("dimension mismatch")
+        bdev = dv.to_device_colmajor(rhs)
+    nrhs = int(bdev.shape[1])
+    if on_device:
+        xd = x.data
+    else:
+        host = np.asarray(x.data)
+        if host.dtype != np.float64:
+            host = host.astype(np.float64)
+        xd = dv.to_device_colmajor(host)
+    L, tau, piv = ltlt_blk_piv_device(xd, b=block or min(DEFAULT_BLOCK, m), fused="var1")
+    if nrhs == 0:
+        out = bdev
+    else:
+        lib = _capi.load()
+        nbytes = lib.skl_ltlt_solve_workspace_size(m, nrhs)
+        ws = dv.workspace(nbytes)
+        info = t.zeros(1, dtype=t.int32, device="cuda")
+        st = lib.skl_ltlt_solve(m, nrhs, L.data_ptr(), dv.ld_of(L), tau.data_ptr() if m > 1 else None,
+                                piv.data_ptr(), bdev.data_ptr(), dv.ld_of(bdev), float(tol_scale), info.data_ptr(),
+                                ws.data_ptr(), nbytes, dv.stream_ptr())
+        _capi.check(st, "solve")
+        code = int(info.item())
+        if code:
+            raise SingularT(f"tridiagonal pivot at row {code - 1}")
+        out = bdev
+    if bd_in is not None:
+        return out.reshape(-1) if one_d else out
+    res = dv.to_host_colmajor(out)
+    return res.ravel() if one_d else res
 
 
 def pfaffian_slog(x: SkewMatrixLower, b=None):

@@ -649,6 +649,24 @@ int skl_ltlt_blk_piv_host(int n, int nb, int variant, const double* X_host, long
 }
 
 // ---------------------------------------------------------------------------
+size_t skl_ltlt_solve_workspace_size(int n, int nrhs) {
+  if (n < 1 || nrhs < 1) return 0;
+  return skl::solve_workspace_bytes(n, nrhs);
+}
+
+int skl_ltlt_solve(int n, int nrhs, const double* L, long long ldl, const double* tau, const long long* piv,
+                   double* B, long long ldb, double tol_scale, int* info, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  if (n < 1 || nrhs < 1 || ldl < n || ldb < n || !L || !piv || !B || !info || (n > 1 && !tau))
+    return SKL_BAD_ARGUMENT;
+  if (workspace_bytes < skl::solve_workspace_bytes(n, nrhs)) return SKL_BAD_ARGUMENT;
+  g_kt.launches += 6 + 4 * ((n + 63) / 64);
+  SKL_TRY(skl::launch_solve(n, nrhs, L, ldl, tau, piv, B, ldb, tol_scale, info, workspace,
+                            static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+// ---------------------------------------------------------------------------
 size_t skl_ltlt_unb_twostep_workspace_size(int n) { return skl::twostep_workspace_bytes(n); }
 
 int skl_ltlt_unb_twostep(int n, int pivot, const double* X, long long ldx, double* L, long long ldl, double* tau,

@@ -91,6 +91,11 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
 int panel_multi_clusters(int csize, size_t smem);
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream);
 
+// linear solve on top of the factorization (solve.cu); B (n x nrhs) is overwritten
+size_t solve_workspace_bytes(int n, int nrhs);
+cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const double* tau, const long long* piv,
+                         double* B, long long ldb, double tol_scale, int* info, void* ws, cudaStream_t stream);
+
 cudaError_t launch_compose_suffix(const int* gperm_all, int npanels, const int* row0s, int n, int* sigma_all,
                                   cudaStream_t stream);
 cudaError_t launch_finalize_l(const double* W, long long ldw, const double* X, long long ldx, double* L,

@@ -1,0 +1,380 @@
+// Linear solve X y = b on top of the pivoted factorization (apps.py:76-100,
+// SURVEY.md 8f rank 2): permute, unit-lower solve, pivoted skew-tridiagonal
+// solve (apps.py:33-73), transposed unit-lower solve, permute back.
+//
+// L is read in the reference's "ones" work-buffer layout: L[i, j] =
+// buf[i, j-1] for i > j >= 1, L[:, 0] = e_0 (core.py:172-220).  The
+// triangular solves are blocked: a one-CTA-per-right-hand-side solve of the
+// 64x64 diagonal block, then a grid-wide update of the remaining rows (one
+// thread per row going down, one warp per row going up so that the column
+// reads of L stay coalesced).  The tridiagonal elimination is factored once by
+// a single thread in the reference's operation order (no FMA contraction),
+// then applied to every right-hand side in parallel (back substitution by the
+// reciprocal pivots).
+#include <cfloat>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace skl {
+namespace {
+
+constexpr int kSolveBlk = 64;
+
+__device__ __forceinline__ double l_at(const double* __restrict__ L, long long ld, int i, int j) {
+  return j >= 1 ? L[(long long)(j - 1) * ld + i] : 0.0;  // i > j
+}
+
+// perm[i] with (P x)[i] = x[perm[i]] (core.py:274-285): the swap chain runs in
+// shared memory (one thread), the result is written out coalesced
+__global__ void compose_perm_kernel(int n, const long long* __restrict__ piv, int* __restrict__ perm) {
+  extern __shared__ int sp[];
+  int* soff = sp + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sp[i] = i;
+    soff[i] = int(piv[i]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < n; ++k) {
+      const int off = soff[k];
+      if (off) {
+        const int j = k + int(off);
+        const int t = sp[k];
+        sp[k] = sp[j];
+        sp[j] = t;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = sp[i];
+}
+
+// dst = src[perm] (gather) or dst[perm] = src (scatter), column-major n x nrhs
+__global__ void permute_rows_kernel(int n, int nrhs, const double* __restrict__ src, long long lds,
+                                    double* __restrict__ dst, long long ldd, const int* __restrict__ perm,
+                                    int scatter) {
+  const long long total = (long long)n * nrhs;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int c = int(e / n), i = int(e - (long long)c * n);
+    if (scatter)
+      dst[(long long)c * ldd + perm[i]] = src[(long long)c * lds + i];
+    else
+      dst[(long long)c * ldd + i] = src[(long long)c * lds + perm[i]];
+  }
+}
+
+// in-place solve of the diagonal block [j0, j1) for right-hand side blockIdx.x;
+// the block of L is staged in shared memory first (one coalesced pass)
+template <bool TRANS>
+__global__ void trsm_diag_kernel(int n, const double* __restrict__ L, long long ld, double* __restrict__ Z,
+                                 long long ldz, int j0, int j1) {
+  __shared__ double lb[kSolveBlk][kSolveBlk + 1];  // lb[col][row] = L[j0+row, j0+col]
+  __shared__ double zb[kSolveBlk];
+  double* z = Z + (long long)blockIdx.x * ldz;
+  const int w = j1 - j0;
+  // column cc of the block (rows j0..j1) is L buffer column j0+cc-1; a warp per column
+  for (int cc = threadIdx.x >> 5; cc < w; cc += blockDim.x >> 5) {
+    const int lane = threadIdx.x & 31;
+    const double* col = j0 + cc >= 1 ? L + (long long)(j0 + cc - 1) * ld + j0 : nullptr;
+    const double v0 = (col && lane > cc && lane < w) ? col[lane] : 0.0;
+    const double v1 = (col && lane + 32 > cc && lane + 32 < w) ? col[lane + 32] : 0.0;
+    lb[cc][lane] = v0;
+    if (lane + 32 < kSolveBlk) lb[cc][lane + 32] = v1;
+  }
+  for (int t = threadIdx.x; t < w; t += blockDim.x) zb[t] = z[j0 + t];
+  __syncthreads();
+  if (!TRANS) {
+    for (int jj = 0; jj < w; ++jj) {
+      const double y = zb[jj];
+      for (int t = jj + 1 + threadIdx.x; t < w; t += blockDim.x) zb[t] -= lb[jj][t] * y;
+      __syncthreads();
+    }
+  } else {
+    for (int jj = w - 1; jj >= 0; --jj) {
+      const double y = zb[jj];
+      for (int t = threadIdx.x; t < jj; t += blockDim.x) zb[t] -= lb[t][jj] * y;
+      __syncthreads();
+    }
+  }
+  for (int t = threadIdx.x; t < w; t += blockDim.x) z[j0 + t] = zb[t];
+}
+
+// rows below the block: z[i] -= sum_{j in [j0,j1)} L[i, j] z[j]   (thread per row,
+// loads of the 64 L entries unrolled so they are in flight together)
+__global__ void trsm_update_down_kernel(int n, int nrhs, const double* __restrict__ L, long long ld,
+                                        double* __restrict__ Z, long long ldz, int j0, int j1) {
+  __shared__ double zb[kSolveBlk];
+  const int c = blockIdx.y;
+  double* z = Z + (long long)c * ldz;
+  const int w = j1 - j0;
+  for (int t = threadIdx.x; t < w; t += blockDim.x) zb[t] = z[j0 + t];
+  __syncthreads();
+  for (int i = j1 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int t = 0;
+    if (w == kSolveBlk) {
+#pragma unroll 16
+      for (; t < kSolveBlk; t += 4) {
+        a0 = fma(l_at(L, ld, i, j0 + t), zb[t], a0);
+        a1 = fma(l_at(L, ld, i, j0 + t + 1), zb[t + 1], a1);
+        a2 = fma(l_at(L, ld, i, j0 + t + 2), zb[t + 2], a2);
+        a3 = fma(l_at(L, ld, i, j0 + t + 3), zb[t + 3], a3);
+      }
+    }
+    for (; t < w; ++t) a0 = fma(l_at(L, ld, i, j0 + t), zb[t], a0);
+    z[i] -= (a0 + a1) + (a2 + a3);
+  }
+}
+
+// rows above the block: z[i] -= sum_{m in [j0,j1)} L[m, i] z[m]   (warp per row)
+__global__ void trsm_update_up_kernel(int n, int nrhs, const double* __restrict__ L, long long ld,
+                                      double* __restrict__ Z, long long ldz, int j0, int j1) {
+  __shared__ double zb[kSolveBlk];
+  const int c = blockIdx.y;
+  double* z = Z + (long long)c * ldz;
+  const int w = j1 - j0;
+  for (int t = threadIdx.x; t < w; t += blockDim.x) zb[t] = z[j0 + t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < j0; i += gridDim.x * wpb) {
+    double acc = 0.0;
+    if (i >= 1) {
+      const double* col = L + (long long)(i - 1) * ld + j0;
+      const double v0 = lane < w ? col[lane] : 0.0;
+      const double v1 = lane + 32 < w ? col[lane + 32] : 0.0;
+      acc = fma(v0, lane < w ? zb[lane] : 0.0, v1 * (lane + 32 < w ? zb[lane + 32] : 0.0));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) z[i] -= acc;
+  }
+}
+
+constexpr int kChunk = 512;  // steps staged in shared memory per round
+
+// factor T (subdiagonal tau) by Gaussian elimination with partial pivoting, one
+// superdiagonal of fill (apps.py:33-73).  The recurrence is sequential: thread
+// 0 runs it in the reference's operation order with the two live rows in
+// registers, while the block stages tau chunks into shared memory and streams
+// the per-step outputs (d, e, f2, multiplier, swap flag) back out coalesced.
+__global__ void tridiag_factor_kernel(int m, const double* __restrict__ tau, double tol_scale, double* d, double* e,
+                                      double* f2, double* mult, int* swp, int* info) {
+  __shared__ double st[kChunk + 1];
+  __shared__ double so[4][kChunk];
+  __shared__ int ss[kChunk];
+  __shared__ double red[32];
+  __shared__ int stop;
+  const int tid = threadIdx.x;
+  double big = 0.0;
+  for (int k = tid; k < m - 1; k += blockDim.x) big = fmax(big, fabs(tau[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) big = fmax(big, __shfl_xor_sync(0xffffffffu, big, o));
+  if ((tid & 31) == 0) red[tid >> 5] = big;
+  if (tid == 0) stop = 0;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < int(blockDim.x >> 5); ++w) big = fmax(big, red[w]);
+    red[0] = big;
+  }
+  __syncthreads();
+  const double thresh = __dmul_rn(__dmul_rn(tol_scale, DBL_EPSILON), red[0]);
+  double dk = 0.0, ek = m > 1 ? -tau[0] : 0.0;  // thread 0's live state
+  for (int k0 = 0; k0 < m - 1; k0 += kChunk) {
+    const int k1 = min(m - 1, k0 + kChunk);
+    for (int t = tid; t <= k1 - k0; t += blockDim.x) st[t] = (k0 + t < m - 1) ? tau[k0 + t] : 0.0;
+    __syncthreads();
+    if (tid == 0) {
+      for (int k = k0; k < k1; ++k) {
+        double sub = st[k - k0];
+        double dk1 = 0.0, ek1 = k + 1 < m - 1 ? -st[k + 1 - k0] : 0.0, f2k = 0.0;
+        int sw = 0;
+        if (fabs(sub) > fabs(dk)) {
+          double t = dk;
+          dk = sub;
+          sub = t;
+          t = ek;
+          ek = dk1;
+          dk1 = t;
+          if (k + 2 < m) {
+            t = f2k;
+            f2k = ek1;
+            ek1 = t;
+          }
+          sw = 1;
+        }
+        if (fabs(dk) <= thresh) {
+          *info = k + 1;
+          stop = 1;
+          break;
+        }
+        const double mu = __dmul_rn(sub, __drcp_rn(dk));  // short dependent chain (tolerance-level vs /)
+        dk1 = __dsub_rn(dk1, __dmul_rn(mu, ek));
+        if (k + 2 < m) ek1 = __dsub_rn(ek1, __dmul_rn(mu, f2k));
+        so[0][k - k0] = dk;
+        so[1][k - k0] = ek;
+        so[2][k - k0] = f2k;
+        so[3][k - k0] = mu;
+        ss[k - k0] = sw;
+        dk = dk1;
+        ek = ek1;
+      }
+    }
+    __syncthreads();
+    if (stop) return;
+    for (int t = tid; t < k1 - k0; t += blockDim.x) {
+      d[k0 + t] = so[0][t];
+      e[k0 + t] = so[1][t];
+      f2[k0 + t] = so[2][t];
+      mult[k0 + t] = so[3][t];
+      swp[k0 + t] = ss[t];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    d[m - 1] = dk;
+    e[m - 1] = ek;
+    f2[m - 1] = 0.0;
+    if (fabs(dk) <= thresh) *info = m;
+  }
+}
+
+// d[k] := 1 / d[k] for the back substitution (multiplications instead of one
+// division per step on the right-hand sides' dependent chain)
+__global__ void tridiag_recip_kernel(int m, double* d, const int* __restrict__ info) {
+  if (*info != 0) return;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) d[k] = 1.0 / d[k];
+}
+
+// apply the factored T to right-hand side blockIdx.x: chunks of the column and
+// of the factor are staged in shared memory, thread 0 runs the recurrences
+__global__ void tridiag_apply_kernel(int m, int nrhs, const double* __restrict__ d, const double* __restrict__ e,
+                                     const double* __restrict__ f2, const double* __restrict__ mult,
+                                     const int* __restrict__ swp, const int* __restrict__ info,
+                                     double* __restrict__ Z, long long ldz) {
+  __shared__ double xs[kChunk + 2];
+  __shared__ double a0[kChunk], a1[kChunk], a2[kChunk];
+  __shared__ int sw[kChunk];
+  if (*info != 0) return;
+  const int tid = threadIdx.x;
+  double* x = Z + (long long)blockIdx.x * ldz;
+  // forward: x[k+1] -= mult[k] x[k] after the optional row swap (k, k+1)
+  double xk = x[0];
+  for (int k0 = 0; k0 < m - 1; k0 += kChunk) {
+    const int k1 = min(m - 1, k0 + kChunk);
+    for (int t = tid; t < k1 - k0; t += blockDim.x) {
+      xs[t] = x[k0 + 1 + t];
+      a0[t] = mult[k0 + t];
+      sw[t] = swp[k0 + t];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int k = k0; k < k1; ++k) {
+        double xk1 = xs[k - k0];
+        if (sw[k - k0]) {
+          const double t = xk;
+          xk = xk1;
+          xk1 = t;
+        }
+        xk1 = __dsub_rn(xk1, __dmul_rn(a0[k - k0], xk));
+        xs[k - k0] = xk;  // final x[k] (slot of x[k+1] reused: x[k] goes out below)
+        xk = xk1;
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < k1 - k0; t += blockDim.x) x[k0 + t] = xs[t];
+    __syncthreads();
+  }
+  if (tid == 0) x[m - 1] = xk;
+  __syncthreads();
+  // back substitution with one extra superdiagonal (d holds 1/d)
+  double xp1 = 0.0, xp2 = 0.0;  // x[k+1], x[k+2] (thread 0)
+  for (int k1 = m; k1 > 0; k1 -= kChunk) {
+    const int k0 = max(0, k1 - kChunk);
+    for (int t = tid; t < k1 - k0; t += blockDim.x) {
+      xs[t] = x[k0 + t];
+      a0[t] = d[k0 + t];
+      a1[t] = e[k0 + t];
+      a2[t] = f2[k0 + t];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int k = k1 - 1; k >= k0; --k) {
+        double v;
+        if (k == m - 1)
+          v = xs[k - k0] * a0[k - k0];
+        else if (k == m - 2)
+          v = __dsub_rn(xs[k - k0], __dmul_rn(a1[k - k0], xp1)) * a0[k - k0];
+        else
+          v = __dsub_rn(__dsub_rn(xs[k - k0], __dmul_rn(a1[k - k0], xp1)), __dmul_rn(a2[k - k0], xp2)) * a0[k - k0];
+        xs[k - k0] = v;
+        xp2 = xp1;
+        xp1 = v;
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < k1 - k0; t += blockDim.x) x[k0 + t] = xs[t];
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+size_t solve_workspace_bytes(int n, int nrhs) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return al(sizeof(int) * n) + al(sizeof(double) * (size_t)n * nrhs) + 4 * al(sizeof(double) * n) +
+         al(sizeof(int) * n);
+}
+
+cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const double* tau, const long long* piv,
+                         double* B, long long ldb, double tol_scale, int* info, void* ws, cudaStream_t stream) {
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  unsigned char* p = static_cast<unsigned char*>(ws);
+  int* perm = reinterpret_cast<int*>(p);
+  p += al(sizeof(int) * n);
+  double* Z = reinterpret_cast<double*>(p);
+  p += al(sizeof(double) * (size_t)n * nrhs);
+  double* d = reinterpret_cast<double*>(p);
+  p += al(sizeof(double) * n);
+  double* e = reinterpret_cast<double*>(p);
+  p += al(sizeof(double) * n);
+  double* f2 = reinterpret_cast<double*>(p);
+  p += al(sizeof(double) * n);
+  double* mult = reinterpret_cast<double*>(p);
+  p += al(sizeof(double) * n);
+  int* swp = reinterpret_cast<int*>(p);
+  const long long ldz = n;
+  cudaError_t err = cudaMemsetAsync(info, 0, sizeof(int), stream);
+  if (err != cudaSuccess) return err;
+  compose_perm_kernel<<<1, 256, 2 * sizeof(int) * n, stream>>>(n, piv, perm);
+  const long long tot = (long long)n * nrhs;
+  const int pg = int(std::min<long long>((tot + 255) / 256, 148 * 8));
+  permute_rows_kernel<<<pg, 256, 0, stream>>>(n, nrhs, B, ldb, Z, ldz, perm, 0);
+  // L z = P b (forward, blocks of 64 columns)
+  for (int j0 = 0; j0 < n; j0 += kSolveBlk) {
+    const int j1 = std::min(n, j0 + kSolveBlk);
+    trsm_diag_kernel<false><<<nrhs, 256, 0, stream>>>(n, L, ldl, Z, ldz, j0, j1);
+    if (j1 < n) {
+      const int rows = n - j1;
+      dim3 grid(std::max(1, std::min((rows + 63) / 64, 148 * 8)), nrhs);
+      trsm_update_down_kernel<<<grid, 64, 0, stream>>>(n, nrhs, L, ldl, Z, ldz, j0, j1);
+    }
+  }
+  tridiag_factor_kernel<<<1, 256, 0, stream>>>(n, tau, tol_scale, d, e, f2, mult, swp, info);
+  tridiag_recip_kernel<<<(n + 255) / 256, 256, 0, stream>>>(n, d, info);
+  tridiag_apply_kernel<<<nrhs, 128, 0, stream>>>(n, nrhs, d, e, f2, mult, swp, info, Z, ldz);
+  // L^T y = z (backward)
+  const int nblk = (n + kSolveBlk - 1) / kSolveBlk;
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int j0 = bi * kSolveBlk, j1 = std::min(n, j0 + kSolveBlk);
+    trsm_diag_kernel<true><<<nrhs, 256, 0, stream>>>(n, L, ldl, Z, ldz, j0, j1);
+    if (j0 > 0) {
+      dim3 grid(std::max(1, std::min((j0 + 7) / 8, 148 * 4)), nrhs);
+      trsm_update_up_kernel<<<grid, 256, 0, stream>>>(n, nrhs, L, ldl, Z, ldz, j0, j1);
+    }
+  }
+  permute_rows_kernel<<<pg, 256, 0, stream>>>(n, nrhs, Z, ldz, B, ldb, perm, 1);
+  return cudaGetLastError();
+}
+
+}  // namespace skl

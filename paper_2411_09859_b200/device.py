@@ -76,3 +76,7 @@ def ld_of(x):
 def vec_to_device(v, dtype):
     t = require_cuda()
     return t.as_tensor(np.ascontiguousarray(np.asarray(v)), device="cuda").to(dtype)
+
+
+def _is_cuda_tensor(x):
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)

@@ -14,6 +14,8 @@ Fixtures
   cfg3_n16384_b256.npz (--big) same for config 3 (about 6 minutes of reference time)
   cfg4_batch.npz       (--big) pfaffian path per matrix (fp64 and fp32): sign, log|Pf| for all 8192,
                        pivots and tau for the first 128
+  solve_small.npz      apps.solve (SURVEY 8f rank 2): n in {2, 8, 64, 300}, 1 and 3 right-hand sides;
+                       SingularT row for odd n
   unpiv_small.npz      unpivoted drivers: ltlt_blk_var1/2a/2b/twostep/left x panel
                        variants ll/rl/twostep, ltlt_unb_rl (+pivoted), ltlt_unb_ll (+first_column),
                        ltlt_unb_panel (ll/rl/twostep, pivoted, first_column) at n in {64, 150, 301}:
@@ -185,6 +187,22 @@ def main():
             put(f"n{n}_panel40_first", sk.ltlt_unb_panel(X, 40, first_column=fcv), n)
         np.savez_compressed(HERE / "unpiv_small.npz", **d)
         print("unpiv ok", flush=True)
+    if want("solve"):
+        d = {}
+        for n in (2, 8, 64, 300):
+            X = sk.SkewMatrixLower(skew_lower(n, n))
+            b1 = np.random.Generator(np.random.Philox(n)).standard_normal(n)
+            b3 = np.random.Generator(np.random.Philox(n + 1)).standard_normal((n, 3))
+            d[f"n{n}_b1"], d[f"n{n}_b3"] = b1, b3
+            d[f"n{n}_y1"], d[f"n{n}_y3"] = sk.solve(X, b1), sk.solve(X, b3)
+        for n in (3, 7):
+            try:
+                sk.solve(sk.SkewMatrixLower(skew_lower(n, n)), np.ones(n))
+                d[f"odd{n}_row"] = np.array(-1)
+            except sk.SingularT as e:
+                d[f"odd{n}_row"] = np.array(int(str(e).rsplit(" ", 1)[-1]))
+        np.savez_compressed(HERE / "solve_small.npz", **d)
+        print("solve ok", flush=True)
     if want("cfg2"):
         g = make_blk(sk, 4096, 128, "var1")
         for fused in ("var2a", "var2b"):

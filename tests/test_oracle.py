@@ -223,3 +223,20 @@ def test_unpivoted_zero_pivot_oracle():
     z[2, 1] = 4.0                        # all-zero first column: tau 0, continue
     r = oracle.ltlt_blk(z, 2, "var1")
     assert r.tau.tolist() == [0.0, 4.0]
+
+
+# ---- solve pinned to the reference ------------------------
+
+@pytest.mark.parametrize("n", [2, 8, 64, 300])
+def test_solve_fixture(golden, n):
+    g = golden("solve_small.npz")
+    x = skew_lower(n, n)
+    assert np.array_equal(oracle.solve(x, g[f"n{n}_b1"]), g[f"n{n}_y1"])
+    assert np.array_equal(oracle.solve(x, g[f"n{n}_b3"]), g[f"n{n}_y3"])
+
+
+@pytest.mark.parametrize("n", [3, 7])
+def test_solve_singular_fixture(golden, n):
+    g = golden("solve_small.npz")
+    with pytest.raises(ZeroDivisionError, match=f"row {int(g[f'odd{n}_row'])}$"):
+        oracle.solve(skew_lower(n, n), np.ones(n))
