@@ -86,6 +86,14 @@ int skl_apply_row_pivots(int n, int q, double* block, long long ld, const long l
 /* apply_symmetric_pivot (core.py:327-333): X := P X P^T, P = (k, k+pi).     */
 int skl_apply_symmetric_pivot(int n, double* X, long long ld, int k, long long pi, void* stream);
 
+/* pack_in_place (core.py:349-362): X[j+1, j] = tau[j], X[j+2:, j] = L[j+2:, j]
+ *   (the LAPACK-style packed factor; only the strictly-lower triangle of X is
+ *   written).  unpack_in_place (core.py:365-375): the exact inverse into a
+ *   fresh "ones" L buffer (every entry written) and tau (n-1); L must not
+ *   alias X.                                                                  */
+int skl_pack_factor(int n, const double* L, long long ldl, const double* tau, double* X, long long ldx, void* stream);
+int skl_unpack_factor(int n, const double* X, long long ldx, double* L, long long ldl, double* tau, void* stream);
+
 /* ---- factorization drivers -------------------------------------------------
  * ltlt_blk_piv (blocked.py:303-363): pivoted blocked right-looking LTL^T.
  *   X (n x n, lower read) is not modified.  L (n x n) receives the work

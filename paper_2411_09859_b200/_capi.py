@@ -35,6 +35,8 @@ SIGNATURES = {
     "skl_apply_row_pivots_workspace_size": (_sz, [_i, _i, _i]),
     "skl_apply_row_pivots": (_i, [_i, _i, _p, _ll, _p, _i, _i, _p, _sz, _p]),
     "skl_apply_symmetric_pivot": (_i, [_i, _p, _ll, _i, _ll, _p]),
+    "skl_pack_factor": (_i, [_i, _p, _ll, _p, _p, _ll, _p]),
+    "skl_unpack_factor": (_i, [_i, _p, _ll, _p, _ll, _p, _p]),
     "skl_ltlt_blk_piv_workspace_size": (_sz, [_i, _i, _i]),
     "skl_ltlt_blk_piv": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _sz, _p]),
     "skl_ltlt_blk": (_i, [_i, _i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),

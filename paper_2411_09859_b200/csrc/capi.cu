@@ -442,6 +442,21 @@ int skl_apply_symmetric_pivot(int n, double* X, long long ld, int k, long long p
   return SKL_OK;
 }
 
+int skl_pack_factor(int n, const double* L, long long ldl, const double* tau, double* X, long long ldx, void* stream) {
+  if (n < 1 || ldl < n || ldx < n) return SKL_BAD_ARGUMENT;
+  g_kt.launches += n > 1 ? 1 : 0;
+  SKL_TRY(skl::launch_pack_factor(n, L, ldl, tau, X, ldx, static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
+int skl_unpack_factor(int n, const double* X, long long ldx, double* L, long long ldl, double* tau, void* stream) {
+  if (n < 1 || ldl < n || ldx < n) return SKL_BAD_ARGUMENT;
+  if (L == X) return SKL_ALIAS;
+  g_kt.launches += 1;
+  SKL_TRY(skl::launch_unpack_factor(n, X, ldx, L, ldl, tau, static_cast<cudaStream_t>(stream)));
+  return SKL_OK;
+}
+
 // ---------------------------------------------------------------------------
 size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant) {
   if (n < 1 || nb < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B) return 0;

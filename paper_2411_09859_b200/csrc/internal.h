@@ -91,6 +91,12 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
 int panel_multi_clusters(int csize, size_t smem);
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream);
 
+// packed factor layout (core.py:349-375)
+cudaError_t launch_pack_factor(int n, const double* L, long long ldl, const double* tau, double* X, long long ldx,
+                               cudaStream_t stream);
+cudaError_t launch_unpack_factor(int n, const double* X, long long ldx, double* L, long long ldl, double* tau,
+                                 cudaStream_t stream);
+
 // linear solve on top of the factorization (solve.cu); B (n x nrhs) is overwritten
 size_t solve_workspace_bytes(int n, int nrhs);
 cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const double* tau, const long long* piv,

@@ -99,7 +99,46 @@ inline dim3 col_grid(int rows, int cols) {
   return dim3(gx, gy);
 }
 
+// packed factor layout (core.py:349-362): X[j+1, j] = tau[j], X[j+2:, j] = L[j+2:, j]
+__global__ void pack_factor_kernel(int n, const double* __restrict__ L, long long ldl, const double* __restrict__ tau,
+                                   double* __restrict__ X, long long ldx) {
+  const int j = blockIdx.y;
+  for (int i = j + 1 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    X[(long long)j * ldx + i] = i == j + 1 ? tau[j] : L[(long long)j * ldl + i];
+}
+
+// exact inverse (core.py:365-375): tau[j] = X[j+1, j]; "ones" L buffer with zeros elsewhere
+__global__ void unpack_factor_kernel(int n, const double* __restrict__ X, long long ldx, double* __restrict__ L,
+                                     long long ldl, double* __restrict__ tau) {
+  const int j = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (j < n - 1) {
+      if (i == j + 1) {
+        v = 1.0;
+        tau[j] = X[(long long)j * ldx + i];
+      } else if (i > j + 1) {
+        v = X[(long long)j * ldx + i];
+      }
+    }
+    L[(long long)j * ldl + i] = v;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_pack_factor(int n, const double* L, long long ldl, const double* tau, double* X, long long ldx,
+                               cudaStream_t stream) {
+  if (n < 2) return cudaSuccess;
+  pack_factor_kernel<<<dim3((n + 255) / 256, n - 1), 256, 0, stream>>>(n, L, ldl, tau, X, ldx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_factor(int n, const double* X, long long ldx, double* L, long long ldl, double* tau,
+                                 cudaStream_t stream) {
+  unpack_factor_kernel<<<dim3((n + 255) / 256, n), 256, 0, stream>>>(n, X, ldx, L, ldl, tau);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_skew_rank2(double* A, long long lda, int n, double alpha, const double* x, const double* y,
                               double beta, cudaStream_t stream) {

@@ -16,6 +16,7 @@ Fixtures
                        pivots and tau for the first 128
   solve_small.npz      apps.solve (SURVEY 8f rank 2): n in {2, 8, 64, 300}, 1 and 3 right-hand sides;
                        SingularT row for odd n
+  mm_small.mtx         mmio.mm_write of a 9x9 skew matrix (the Matrix Market format)
   unpiv_small.npz      unpivoted drivers: ltlt_blk_var1/2a/2b/twostep/left x panel
                        variants ll/rl/twostep, ltlt_unb_rl (+pivoted), ltlt_unb_ll (+first_column),
                        ltlt_unb_panel (ll/rl/twostep, pivoted, first_column) at n in {64, 150, 301}:
@@ -203,6 +204,11 @@ def main():
                 d[f"odd{n}_row"] = np.array(int(str(e).rsplit(" ", 1)[-1]))
         np.savez_compressed(HERE / "solve_small.npz", **d)
         print("solve ok", flush=True)
+    if want("mmio"):
+        x = sk.SkewMatrixLower(skew_lower(9, 4))
+        x.data[5, 2] = 0.0                           # a structural zero is skipped
+        sk.mm_write(HERE / "mm_small.mtx", x)
+        print("mmio ok", flush=True)
     if want("cfg2"):
         g = make_blk(sk, 4096, 128, "var1")
         for fused in ("var2a", "var2b"):
