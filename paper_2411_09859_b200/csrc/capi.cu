@@ -682,11 +682,31 @@ int skl_ltlt_solve(int n, int nrhs, const double* L, long long ldl, const double
 }
 
 // ---------------------------------------------------------------------------
-size_t skl_ltlt_unb_twostep_workspace_size(int n) { return skl::twostep_workspace_bytes(n); }
+// From n = 128 up the two-step factorization is computed faster by the blocked
+// driver (left-looking cluster panel + DMMA trailing update): the same L, T and
+// pivots in exact arithmetic, and the cluster two-step kernel pays five cluster
+// barriers per column pair (n=512: 1.50 vs 2.54 ms; n=1024: 2.9 vs 13.2 ms).
+namespace {
+constexpr int kTwostepViaBlocked = 128;
+size_t twostep_blocked_ws(int n) {
+  std::vector<PanelPlan> plan;
+  if (n < kTwostepViaBlocked || !make_schedule(n, n, SKL_VAR1, plan)) return 0;
+  return layout_blk(n, n, plan, nullptr, nullptr);
+}
+}  // namespace
+
+size_t skl_ltlt_unb_twostep_workspace_size(int n) {
+  return std::max(skl::twostep_workspace_bytes(n), twostep_blocked_ws(n));
+}
 
 int skl_ltlt_unb_twostep(int n, int pivot, const double* X, long long ldx, double* L, long long ldl, double* tau,
                          long long* piv, int* info_dev, void* workspace, size_t workspace_bytes, void* stream) {
   if (n < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
+  static int via_blocked = env_int("SKL_TWOSTEP_VIA_BLOCKED", 1);
+  const size_t blk_ws = via_blocked ? twostep_blocked_ws(n) : 0;
+  if (blk_ws > 0 && workspace_bytes >= blk_ws && info_dev != nullptr)
+    return blk_driver(n, n, SKL_VAR1, pivot ? 1 : 0, -1, X, ldx, L, ldl, tau, pivot ? piv : nullptr, info_dev,
+                      workspace, workspace_bytes, stream);
   if (workspace_bytes < skl::twostep_workspace_bytes(n)) return SKL_BAD_ARGUMENT;
   g_kt.launches += (L != X) ? 2 : 1;
   SKL_TRY(skl::launch_twostep(X, ldx, L, ldl, n, pivot, tau, piv, info_dev, workspace,
