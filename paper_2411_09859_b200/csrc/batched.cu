@@ -20,7 +20,13 @@
 namespace skl {
 namespace {
 
-constexpr int kBThreads = 512;
+#ifndef SKL_BATCHED_THREADS
+#define SKL_BATCHED_THREADS 256
+#endif
+#ifndef SKL_BATCHED_PER_SM
+#define SKL_BATCHED_PER_SM 3
+#endif
+constexpr int kBThreads = SKL_BATCHED_THREADS;
 constexpr int kBWarps = kBThreads / 32;
 constexpr size_t kRedBytes = 2 * kBWarps * (sizeof(double) + sizeof(int));
 
@@ -173,7 +179,7 @@ namespace {
 #endif
 
 template <typename T>
-__global__ void __launch_bounds__(kBThreads, 1)
+__global__ void __launch_bounds__(kBThreads, SKL_BATCHED_PER_SM)
 batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx, long long strideX, T* __restrict__ L,
                long long ldl, long long strideL, T* __restrict__ tau, long long strideTau, long long* __restrict__ piv,
                long long stridePiv, double* __restrict__ pf_sign, double* __restrict__ pf_logabs) {
@@ -357,12 +363,15 @@ cudaError_t launch_batched(int batch, int n, const T* X, long long ldx, long lon
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // SKL_BATCHED_PER_SM matrices share an SM (each CTA gets 1/k of the shared memory)
+  const size_t budget = SKL_BATCHED_PER_SM == 1 ? (size_t)lim : (size_t)(228 * 1024) / SKL_BATCHED_PER_SM - 1024;
   int J0 = 0;
-  while (J0 < n - 1 && batched_smem<T>(n, J0) > (size_t)lim) ++J0;
+  while (J0 < n - 1 && batched_smem<T>(n, J0) > budget) ++J0;
   size_t smem = batched_smem<T>(n, J0);
   cudaError_t e = cudaFuncSetAttribute(batched_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int grid = batch < nsm ? batch : nsm;
+  long long g = (long long)nsm * SKL_BATCHED_PER_SM;
+  int grid = batch < g ? batch : (int)g;
   batched_kernel<T><<<grid, kBThreads, smem, stream>>>(batch, n, J0, X, ldx, strideX, L, ldl, strideL, tau, strideTau,
                                                        piv, stridePiv, pf_sign, pf_logabs);
   return cudaGetLastError();
