@@ -554,6 +554,7 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
         SKL_TRY(skl::launch_panel_cluster(a, st));
       else
         SKL_TRY(skl::launch_panel(a, st));
+      if (p.cluster != 0) g_kt.launches += 2;  // + panel_finish_gather / panel_finish_write
     }
     tag += (uint32_t)p.nelim + 1;
 
