@@ -241,6 +241,30 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def panel_dram_traffic(path=Path(__file__).resolve().parent / "profiles" / "r01_panel_dram_n4096.csv"):
+    """Mean DRAM bytes (read + write) per panel_cluster_kernel launch of one config-2
+    factorization, from the committed ncu capture (``ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum -k regex:panel_cluster python tools/run_blk.py --reps 1``; the
+    second factorization's launches).  None when the capture is absent."""
+    import csv
+    if not path.exists():
+        return None
+    rows = list(csv.reader(path.read_text().splitlines()))
+    hi = next((i for i, r in enumerate(rows) if r and r[0] == "ID"), None)
+    if hi is None:
+        return None
+    ci = {x: i for i, x in enumerate(rows[hi])}
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    per = {}
+    for r in rows[hi + 1:]:
+        m = r[ci["Metric Name"]]
+        if m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            per[int(r[ci["ID"]])] = per.get(int(r[ci["ID"]]), 0.0) + float(r[ci["Metric Value"]]) * scale.get(
+                r[ci["Metric Unit"]], 1.0)
+    ids = sorted(per)[len(per) // 2:]
+    return int(sum(per[i] for i in ids) / len(ids)) if ids else None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -356,7 +380,7 @@ def main():
         ach = per_launch_bytes / per_launch_s / 1e9
         roof = {"kernel": "panel_cluster_kernel (pivoted left-looking panel)", "bound": "hbm",
                 "achieved": round(ach, 2), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
-                "traffic": None, "peak_source": peak_src,
+                "traffic": panel_dram_traffic(), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(per_launch_bytes), "launches_per_step": cnt["panel"]}
     gemm_tf = fc.level3 / (per_fact["trailing_gemm"] * 1e-3) / 1e12 if per_fact["trailing_gemm"] else None
 
