@@ -168,6 +168,64 @@ int skl_ltlt_batched_piv(int batch, int n, int dtype, const void* X, long long l
                          long long ldl, long long strideL, void* tau, long long* piv, double* pf_sign,
                          double* pf_logabs, void* stream);
 
+/* ---- block-cyclic multi-GPU factorization (config 5) ----------
+ * The reference has no distributed path; this is the GPU counterpart of
+ * ltlt_blk_piv (blocked.py:303-363) over G ranks, one process per GPU.
+ *
+ * W (n x n, column stride ldw) is ONE virtual address range on every rank in
+ *   which column block j = [j*nbd, (j+1)*nbd) is backed by the memory of rank
+ *   j % G (skl_vmm_* below; the host layer maps it).  On entry every rank's
+ *   blocks hold X's lower triangle; W is the work buffer (destroyed).
+ * L (same block-cyclic mapping, stride ldl) receives, for the columns this
+ *   process drives, the "ones" L buffer of skl_ltlt_blk_piv (strict lower part).
+ * shared (skl_ltlt_dist_shared_size bytes, one range visible to all ranks):
+ *   tau (n-1 doubles) at off_tau and piv (n int64) at off_piv
+ *   (skl_ltlt_dist_offsets); the rest is panel state.
+ * Ranks [rank_lo, rank_hi) are driven by this process: one rank per process on
+ *   a multi-GPU node (barrier required: a stream-ordered cross-rank barrier,
+ *   e.g. skl_nccl_barrier), or all G ranks in one process on one device (no
+ *   barrier; the same kernels with every rank's column filter).
+ * Per panel: the owner of the panel's first column runs the pivoted panel
+ *   (pivot-column gathers and interchanges over peer memory), barrier, every
+ *   rank packs the panel operands and updates the trailing columns it owns
+ *   (column-filtered DMMA GEMM), barrier.                                     */
+typedef int (*skl_barrier_fn)(void* ctx, void* stream);
+size_t skl_ltlt_dist_shared_size(int n, int nb, int variant);
+size_t skl_ltlt_dist_workspace_size(int n, int nb, int variant, int nranks_local);
+int skl_ltlt_dist_offsets(int n, int nb, int variant, size_t* off_tau, size_t* off_piv, size_t* off_gperm,
+                          int* npanels);
+int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int rank_lo, int rank_hi, double* W,
+                          long long ldw, double* L, long long ldl, void* shared, void* workspace,
+                          size_t workspace_bytes, skl_barrier_fn barrier, void* barrier_ctx, void* stream);
+/* host only: owned-tile table of the column-filtered trailing GEMM (the lower
+ *   triangle of an n x n region whose column 0 is global column cbase):
+ *   tab = [m, total, (tile column, first tile, partial) x m]; tab_ints >=
+ *   2 + 3*ceil(n/128).                                                        */
+int skl_dist_owner_table(int n, long long cbase, int nbd, int nranks, int rank, int* tab, size_t tab_ints);
+
+/* CUDA VMM plumbing (driver API through cudaGetDriverEntryPoint): physical
+ * allocations (exportable as POSIX fds for the peer processes), virtual ranges,
+ * block mapping with read/write access for `device`.                        */
+int skl_vmm_available(void);
+int skl_vmm_last_result(void); /* CUresult of the last skl_vmm_* driver call */
+int skl_vmm_granularity(int device, size_t* gran);
+int skl_vmm_create(size_t bytes, int device, int exportable, unsigned long long* handle);
+int skl_vmm_export_fd(unsigned long long handle, int* fd);
+int skl_vmm_import_fd(int fd, unsigned long long* handle);
+int skl_vmm_release(unsigned long long handle);
+int skl_vmm_reserve(size_t bytes, size_t align, unsigned long long* va);
+int skl_vmm_free_va(unsigned long long va, size_t bytes);
+int skl_vmm_map(unsigned long long va, size_t bytes, unsigned long long handle, size_t offset, int device);
+int skl_vmm_unmap(unsigned long long va, size_t bytes);
+
+/* NCCL stream-ordered barrier (libnccl.so.2 via dlopen): a one-word
+ * all-reduce on the caller's stream; skl_nccl_barrier matches skl_barrier_fn. */
+int skl_nccl_available(void);
+int skl_nccl_unique_id(unsigned char* out, size_t bytes);
+int skl_nccl_barrier_create(int nranks, int rank, const unsigned char* id, void** ctx);
+int skl_nccl_barrier(void* ctx, void* stream);
+int skl_nccl_barrier_destroy(void* ctx);
+
 /* ---- instrumentation (bench / profiling) ---------------------------------
  * skl_timing_enable(1) records CUDA events around every kernel the blocked
  * driver launches, by class (0 panel, 1 operand pack, 2 trailing GEMM,

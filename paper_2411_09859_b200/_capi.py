@@ -49,11 +49,36 @@ SIGNATURES = {
     "skl_ltlt_unb_twostep_workspace_size": (_sz, [_i]),
     "skl_ltlt_unb_twostep": (_i, [_i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
     "skl_ltlt_batched_piv": (_i, [_i, _i, _i, _p, _ll, _ll, _p, _ll, _ll, _p, _p, _p, _p, _p]),
+    "skl_ltlt_dist_shared_size": (_sz, [_i, _i, _i]),
+    "skl_ltlt_dist_workspace_size": (_sz, [_i, _i, _i, _i]),
+    "skl_ltlt_dist_offsets": (_i, [_i, _i, _i, _p, _p, _p, _p]),
+    "skl_ltlt_blk_piv_dist": (_i, [_i, _i, _i, _i, _i, _i, _i, _p, _ll, _p, _ll, _p, _p, _sz, _p, _p, _p]),
+    "skl_dist_owner_table": (_i, [_i, _ll, _i, _i, _i, _p, _sz]),
+    "skl_vmm_available": (_i, []),
+    "skl_vmm_last_result": (_i, []),
+    "skl_vmm_granularity": (_i, [_i, _p]),
+    "skl_vmm_create": (_i, [_sz, _i, _i, _p]),
+    "skl_vmm_export_fd": (_i, [C.c_ulonglong, _p]),
+    "skl_vmm_import_fd": (_i, [_i, _p]),
+    "skl_vmm_release": (_i, [C.c_ulonglong]),
+    "skl_vmm_reserve": (_i, [_sz, _sz, _p]),
+    "skl_vmm_free_va": (_i, [C.c_ulonglong, _sz]),
+    "skl_vmm_map": (_i, [C.c_ulonglong, _sz, C.c_ulonglong, _sz, _i]),
+    "skl_vmm_unmap": (_i, [C.c_ulonglong, _sz]),
+    "skl_nccl_available": (_i, []),
+    "skl_nccl_unique_id": (_i, [_p, _sz]),
+    "skl_nccl_barrier_create": (_i, [_i, _i, _p, _p]),
+    "skl_nccl_barrier": (_i, [_p, _p]),
+    "skl_nccl_barrier_destroy": (_i, [_p]),
     "skl_timing_enable": (_i, [_i]),
     "skl_timing_read": (_i, [_p, _p]),
     "skl_launch_count": (_ll, []),
     "skl_debug_set_panel_profile": (_i, [_p]),
 }
+
+
+#: C type of skl_barrier_fn (a host callback may implement the cross-rank barrier)
+BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
 
 
 class NativeUnavailable(RuntimeError):

@@ -585,6 +585,253 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
 }
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Block-cyclic multi-GPU driver (config 5).  The work matrix W is
+// ONE virtual address range on every rank whose nbd-column blocks are backed by
+// the HBM of rank (block % G) (CUDA VMM, mapped by the host layer), so the
+// panel kernels address remote columns exactly like local ones over NVLink.
+// Per panel: the owner of the panel's first column runs the pivoted panel and
+// its finish kernels (pivot-column gathers and interchanges read/write peer
+// memory); barrier; every rank packs the panel operands and runs the DMMA
+// trailing GEMM on the columns it owns; barrier.  tau / piv / y / gperm live
+// in a shared region (one rank's memory, mapped by all).
+namespace {
+struct DistShared {
+  double* tau;
+  long long* piv;
+  double* y;
+  int* gperm_all;
+};
+size_t layout_dist_shared(int n, int np, void* base, DistShared* out) {
+  Bump b(base);
+  DistShared d{};
+  d.tau = b.take<double>(n);
+  d.piv = b.take<long long>(n);
+  d.y = b.take<double>(n);
+  d.gperm_all = b.take<int>((size_t)std::max(np, 1) * n);
+  if (out) *out = d;
+  return b.off + 256;
+}
+struct DistWs {
+  BlkWorkspace blk;  // W unused (the global matrix is the caller's)
+  int* own_tab;      // [np][nr][owner_table_ints(n)]
+  size_t tab_stride;
+};
+size_t layout_dist(int n, int nb, int nr, const std::vector<PanelPlan>& plan, void* base, DistWs* ws) {
+  Bump b(base);
+  int kmax = 1, nelim_max = 1, ctas = 1;
+  for (auto& p : plan) {
+    kmax = std::max(kmax, p.kmax);
+    nelim_max = std::max(nelim_max, p.nelim);
+    ctas = std::max(ctas, p.ctas);
+  }
+  (void)nb;
+  const int np = (int)plan.size();
+  BlkWorkspace w{};
+  const int k4cap = (kmax + 2 + 3) / 4;
+  const int slot_words = 4 + 2 * (kmax + 2);
+  w.W = nullptr;
+  w.pbuf = b.take<double>((size_t)kmax * n);
+  w.P = b.take<double>(skl::packed_elems(n, k4cap));
+  w.Q = b.take<double>(skl::packed_elems(n, k4cap));
+  w.side = b.take<double>((size_t)2 * (nelim_max + 1) * n);
+  w.sigma_all = b.take<int>((size_t)std::max(np, 1) * n);
+  w.col_group = b.take<int>(n);
+  w.disp_list = b.take<int>(2 * (nelim_max + 1));
+  w.disp_count = b.take<int>(1);
+  size_t ll_start = align_up(b.off);
+  w.slots = b.take<uint64_t>((size_t)ctas * 2 * slot_words);
+  w.rowa = b.take<uint64_t>((size_t)2 * slot_words);
+  w.recs = b.take<uint64_t>((size_t)2 * ctas * 4);
+  w.crow = b.take<double>((size_t)2 * 16 * (kmax + 2));
+  w.arowg = b.take<double>((size_t)2 * (kmax + 2));
+  w.ll_bytes = b.off - ll_start;
+  w.k4cap = k4cap;
+  w.slot_words = slot_words;
+  w.np = np;
+  DistWs d{};
+  d.blk = w;
+  d.tab_stride = skl::owner_table_ints(n);
+  d.own_tab = b.take<int>((size_t)std::max(np, 1) * nr * d.tab_stride);
+  if (ws) *ws = d;
+  return b.off + 256;
+}
+}  // namespace
+
+size_t skl_ltlt_dist_shared_size(int n, int nb, int variant) {
+  if (n < 2 || nb < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B) return 0;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, nb, variant, plan)) return 0;
+  return layout_dist_shared(n, (int)plan.size(), nullptr, nullptr);
+}
+
+size_t skl_ltlt_dist_workspace_size(int n, int nb, int variant, int nranks_local) {
+  if (n < 2 || nb < 1 || nranks_local < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B) return 0;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, nb, variant, plan)) return 0;
+  return layout_dist(n, nb, nranks_local, plan, nullptr, nullptr);
+}
+
+int skl_ltlt_dist_offsets(int n, int nb, int variant, size_t* off_tau, size_t* off_piv, size_t* off_gperm,
+                          int* npanels) {
+  std::vector<PanelPlan> plan;
+  if (n < 2 || nb < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B || !make_schedule(n, nb, variant, plan))
+    return SKL_BAD_ARGUMENT;
+  DistShared d;
+  layout_dist_shared(n, (int)plan.size(), reinterpret_cast<void*>(uintptr_t(0x100000)), &d);
+  const uintptr_t b0 = 0x100000;
+  if (off_tau) *off_tau = reinterpret_cast<uintptr_t>(d.tau) - b0;
+  if (off_piv) *off_piv = reinterpret_cast<uintptr_t>(d.piv) - b0;
+  if (off_gperm) *off_gperm = reinterpret_cast<uintptr_t>(d.gperm_all) - b0;
+  if (npanels) *npanels = (int)plan.size();
+  return SKL_OK;
+}
+
+int skl_dist_owner_table(int n, long long cbase, int nbd, int nranks, int rank, int* tab, size_t tab_ints) {
+  if (n < 1 || nbd < 1 || nranks < 1 || rank < 0 || rank >= nranks || !tab) return SKL_BAD_ARGUMENT;
+  if (tab_ints < skl::owner_table_ints(n)) return SKL_BAD_ARGUMENT;
+  return skl::build_owner_table(n, cbase, nbd, nranks, rank, tab) >= 0 ? SKL_OK : SKL_BAD_ARGUMENT;
+}
+
+int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int rank_lo, int rank_hi, double* W,
+                          long long ldw, double* L, long long ldl, void* shared, void* workspace,
+                          size_t workspace_bytes, skl_barrier_fn barrier, void* barrier_ctx, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (variant < SKL_VAR1 || variant > SKL_VAR2B) return SKL_UNSUPPORTED;
+  if (n < 2 || nb < 1 || nbd < 1 || nranks < 1 || rank_lo < 0 || rank_hi > nranks || rank_lo >= rank_hi ||
+      ldw < n || ldl < n || !W || !L || !shared || !workspace)
+    return SKL_BAD_ARGUMENT;
+  const bool all_local = rank_lo == 0 && rank_hi == nranks;
+  if (!all_local && !barrier) return SKL_BAD_ARGUMENT;
+  const int nr = rank_hi - rank_lo;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, nb, variant, plan)) {
+    g_last_error = "panel block does not fit the shared-memory budget";
+    return SKL_UNSUPPORTED;
+  }
+  const int np = (int)plan.size();
+  if (workspace_bytes < layout_dist(n, nb, nr, plan, nullptr, nullptr)) return SKL_BAD_ARGUMENT;
+  DistWs dw;
+  layout_dist(n, nb, nr, plan, workspace, &dw);
+  BlkWorkspace& ws = dw.blk;
+  DistShared sh;
+  layout_dist_shared(n, np, shared, &sh);
+  auto sync = [&]() -> int {
+    if (all_local) return SKL_OK;
+    const int rc = barrier(barrier_ctx, stream);
+    if (rc != 0) {
+      g_last_error = "distributed barrier failed";
+      return SKL_CUDA_ERROR;
+    }
+    return SKL_OK;
+  };
+
+  // host tables: column -> last panel containing it; per (panel, rank) owned GEMM tiles
+  std::vector<int> group(n, 0);
+  for (int k = 0; k < np; ++k)
+    for (int c = plan[k].lo; c < n; ++c) group[c] = k;
+  std::vector<int> tabs((size_t)np * nr * dw.tab_stride, 0);
+  std::vector<int> ntiles((size_t)np * nr, 0);
+  for (int k = 0; k < np; ++k) {
+    const int rt = plan[k].r + plan[k].nelim;
+    if (n - rt < 2) continue;
+    for (int q = 0; q < nr; ++q)
+      ntiles[(size_t)k * nr + q] = skl::build_owner_table(n - rt, rt, nbd, nranks, rank_lo + q,
+                                                          tabs.data() + ((size_t)k * nr + q) * dw.tab_stride);
+  }
+  SKL_TRY(cudaMemcpyAsync(ws.col_group, group.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  SKL_TRY(cudaMemcpyAsync(dw.own_tab, tabs.data(), sizeof(int) * tabs.size(), cudaMemcpyHostToDevice, st));
+  SKL_TRY(cudaMemsetAsync(ws.slots, 0, ws.ll_bytes, st));
+  if (rank_lo == 0) {
+    SKL_TRY(cudaMemsetAsync(sh.tau, 0, sizeof(double) * (n - 1), st));
+    SKL_TRY(cudaMemsetAsync(sh.piv, 0, sizeof(long long) * n, st));
+  }
+  // the host tables are pageable: the copies above complete before this returns
+  int rc = sync();
+  if (rc) return rc;
+
+  uint32_t tag = 1;
+  for (int k = 0; k < np; ++k) {
+    const PanelPlan& p = plan[k];
+    const int rt = p.r + p.nelim;
+    const bool straggler = (variant == SKL_VAR1) && (n - rt >= 2);
+    const int runner = (p.r / nbd) % nranks;
+    if (runner >= rank_lo && runner < rank_hi) {
+      skl::PanelArgs a{};
+      a.W = W;
+      a.ld = ldw;
+      a.n = n;
+      a.r = p.r;
+      a.nelim = p.nelim;
+      a.lo = p.lo;
+      a.want_y = straggler ? 1 : 0;
+      a.tau = sh.tau;
+      a.piv = sh.piv;
+      a.y = sh.y;
+      a.gperm = sh.gperm_all + (size_t)k * n;
+      a.disp_list = ws.disp_list;
+      a.disp_count = ws.disp_count;
+      a.side = ws.side;
+      a.slots = ws.slots;
+      a.rowa = ws.rowa;
+      a.recs = ws.recs;
+      a.crow = ws.crow;
+      a.arowg = ws.arowg;
+      a.pbuf = ws.pbuf;
+      a.tag0 = tag;
+      a.nblocks = p.ctas;
+      a.rows_per = p.rows_per;
+      a.kmax = p.kmax;
+      a.slot_words = ws.slot_words;
+      a.prof = nullptr;
+      a.pivot = 1;
+      a.info = nullptr;
+      KScope ks(KPANEL, st);
+      if (p.cluster == 2)
+        SKL_TRY(skl::launch_panel_multi(a, p.csize, st));
+      else if (p.cluster == 1)
+        SKL_TRY(skl::launch_panel_cluster(a, st));
+      else
+        SKL_TRY(skl::launch_panel(a, st));
+      if (p.cluster != 0) g_kt.launches += 2;
+    }
+    tag += (uint32_t)p.nelim + 1;  // every process advances the LL tag identically
+    if ((rc = sync())) return rc;
+
+    const int ntr = n - rt;
+    if (ntr >= 2) {
+      const int ka = rt - p.lo;
+      const int K = ka + (straggler ? 2 : 0);
+      const int nk4 = (K + 3) / 4;
+      {
+        KScope ks(KPACK, st);
+        SKL_TRY(skl::launch_pack_rankk(W + (size_t)p.lo * ldw + rt, ldw, ntr, ka, sh.tau + p.lo + 1, -1.0,
+                                       straggler ? sh.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st));
+      }
+      for (int q = 0; q < nr; ++q) {
+        const int nt = ntiles[(size_t)k * nr + q];
+        if (nt == 0) continue;
+        skl::ColOwner own{dw.own_tab + ((size_t)k * nr + q) * dw.tab_stride, nt, (long long)rt, nbd, nranks,
+                          rank_lo + q};
+        KScope ks(KGEMM, st);
+        SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, W + (size_t)rt * ldw + rt, ldw, ntr, 1.0,
+                                       st, &own));
+      }
+      if ((rc = sync())) return rc;
+    }
+  }
+  {
+    KScope ks(KFINAL, st);
+    SKL_TRY(skl::launch_compose_suffix(sh.gperm_all, np, nullptr, n, ws.sigma_all, st));
+    for (int q = 0; q < nr; ++q) {
+      g_kt.launches++;
+      SKL_TRY(skl::launch_finalize_l(W, ldw, W, ldw, L, ldl, n, ws.col_group, ws.sigma_all, 0, st, nbd, nranks,
+                                     rank_lo + q));
+    }
+  }
+  return sync();
+}
+
 int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
                      double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream) {
   return blk_driver(n, nb, variant, 1, -1, X, ldx, L, ldl, tau, piv, nullptr, workspace, workspace_bytes, stream);

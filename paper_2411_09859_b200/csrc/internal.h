@@ -16,10 +16,26 @@ constexpr int kTile = 128;
 __host__ __device__ inline int tiles_for(int rows) { return (rows + kTile - 1) / kTile; }
 __host__ __device__ inline size_t packed_elems(int rows, int k4cap) { return (size_t)tiles_for(rows) * kTile * 4 * k4cap; }
 
+// Block-cyclic column ownership of a GEMM launch (multi-GPU driver): only C
+// columns c (global index cbase + c) with (c / nbd) % G == rank are written;
+// tab (device) is the owned-tile table build_owner_table() fills.
+struct ColOwner {
+  const int* tab;
+  int ntiles;
+  long long cbase;
+  int nbd, G, rank;
+};
+// host: owned-tile table for the lower triangle of an n x n region whose column
+// 0 is global column cbase; tab needs 2 + 3*tiles_for(n) ints; returns the tile count
+int build_owner_table(int n, long long cbase, int nbd, int G, int rank, int* tab);
+inline size_t owner_table_ints(int n) { return 2 + 3 * (size_t)tiles_for(n); }
+
 // C[i,j] (i>j, i,j < n) = beta*C[i,j] + sum_k P[i,k] Q[j,k]
-// nk4_dev (optional) overrides nk4 with a device-resident count.
+// nk4_dev (optional) overrides nk4 with a device-resident count; own (optional)
+// restricts the update to one rank's columns.
 cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
-                              double* C, long long ldc, int n, double beta, cudaStream_t stream);
+                              double* C, long long ldc, int n, double beta, cudaStream_t stream,
+                              const ColOwner* own = nullptr);
 
 // P = alpha*A, Q = A T^T with T tridiag(t) (t = tau_base[0..ka-2]); optional
 // var1 straggler columns (l = A[:, ka-1], y) zeroed on row 0.
@@ -104,9 +120,10 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
 
 cudaError_t launch_compose_suffix(const int* gperm_all, int npanels, const int* row0s, int n, int* sigma_all,
                                   cudaStream_t stream);
+// own_g > 1: only the columns c with (c / own_nbd) % own_g == own_rank
 cudaError_t launch_finalize_l(const double* W, long long ldw, const double* X, long long ldx, double* L,
                               long long ldl, int n, const int* col_group, const int* sigma_all, int copy_upper,
-                              cudaStream_t stream);
+                              cudaStream_t stream, int own_nbd = 1, int own_g = 1, int own_rank = 0);
 
 // ---- unblocked two-step (config 1) and batched (config 4) ------------------
 cudaError_t launch_twostep(const double* X, long long ldx, double* L, long long ldl, int n, int pivot,

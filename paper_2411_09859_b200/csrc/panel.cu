@@ -509,8 +509,9 @@ __global__ void compose_suffix_kernel(const int* __restrict__ gperm_all, int np,
 __global__ void finalize_l_kernel(const double* __restrict__ W, long long ldw, const double* __restrict__ X,
                                   long long ldx, double* __restrict__ L, long long ldl, int n,
                                   const int* __restrict__ col_group, const int* __restrict__ sigma_all,
-                                  int copy_upper) {
+                                  int copy_upper, int own_nbd, int own_g, int own_rank) {
   for (int c = blockIdx.y; c < n; c += gridDim.y) {
+    if (own_g > 1 && (c / own_nbd) % own_g != own_rank) continue;  // another rank's column
     const int grp = col_group[c];
     const int* sg = sigma_all + (size_t)grp * n;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -562,9 +563,10 @@ cudaError_t launch_compose_suffix(const int* gperm_all, int npanels, const int* 
 
 cudaError_t launch_finalize_l(const double* W, long long ldw, const double* X, long long ldx, double* L,
                               long long ldl, int n, const int* col_group, const int* sigma_all, int copy_upper,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, int own_nbd, int own_g, int own_rank) {
   dim3 grid((n + 255) / 256 < 8 ? (n + 255) / 256 : 8, n < 4096 ? n : 4096);
-  finalize_l_kernel<<<grid, 256, 0, stream>>>(W, ldw, X, ldx, L, ldl, n, col_group, sigma_all, copy_upper);
+  finalize_l_kernel<<<grid, 256, 0, stream>>>(W, ldw, X, ldx, L, ldl, n, col_group, sigma_all, copy_upper, own_nbd,
+                                              own_g, own_rank);
   return cudaGetLastError();
 }
 

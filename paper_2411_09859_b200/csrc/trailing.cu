@@ -18,6 +18,7 @@
 // Only lower tiles are launched (triangle-aware schedule); diagonal tiles
 // mask i <= j at load and store, so the upper triangle is never read or
 // written (test_core.py:39-58 NaN-poison invariant).
+#include <algorithm>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -90,6 +91,24 @@ __host__ __device__ __forceinline__ void lower_tile_swizzled(int t, int nt, int&
   ti = tj + u;
 }
 
+// Column-owned subset of the lower tiles (block-cyclic multi-GPU driver): tab =
+// [m, total, (tcol, first, partial) x m] lists the tile columns holding at least
+// one column this rank owns; tile t maps to column c with first[c] <= t <
+// first[c+1] and row tj + (t - first[c]).  `partial` tiles straddle a
+// distribution-block boundary and take the column-masked register epilogue.
+__device__ __forceinline__ void owned_tile(const int* __restrict__ tab, int t, int& ti, int& tj, int& part) {
+  const int m = tab[0];
+  const int* e = tab + 2;
+  int lo = 0, hi = m - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (e[3 * mid + 1] <= t) lo = mid; else hi = mid - 1;
+  }
+  tj = e[3 * lo];
+  ti = tj + (t - e[3 * lo + 1]);
+  part = e[3 * lo + 2];
+}
+
 // Persistent lower-triangular DGEMM-NT: one CTA per SM walks the lower tiles
 // (ti >= tj) round-robin; the bulk-copy ring runs ahead across tile
 // boundaries so the next tile's operands stream in during the epilogue.  The
@@ -98,7 +117,8 @@ __host__ __device__ __forceinline__ void lower_tile_swizzled(int t, int nt, int&
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, const double* __restrict__ P,
                      const double* __restrict__ Q, int k4cap, int nk4_host,
-                     const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta) {
+                     const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta,
+                     const int* __restrict__ own_tab, long long own_cbase, int own_nbd, int own_g, int own_rank) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 1 KiB-align the carve-up (the swizzled boxes need it)
   unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -113,7 +133,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
   // the next tile's MMAs; diagonal tiles keep the masked register epilogue
   const bool bulk_ok = use_tmap && beta == 1.0;
   const int nt = tiles_for(n);
-  const int ntiles = nt * (nt + 1) / 2;
+  const int ntiles = own_tab ? own_tab[1] : nt * (nt + 1) / 2;
   const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
   const int nchunks = (nk4 + kK4PerStage - 1) / kK4PerStage;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -121,8 +141,9 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int total_chunks = my_tiles * nchunks;
   if (my_tiles == 0 || nchunks == 0) {
-    // nothing to multiply: still apply beta to the owned tiles
-    for (int t = blockIdx.x; t < ntiles && nchunks == 0; t += gridDim.x) {
+    // nothing to multiply: still apply beta to the owned tiles (the column-owned
+    // launches always carry K >= 1)
+    for (int t = blockIdx.x; t < ntiles && nchunks == 0 && !own_tab; t += gridDim.x) {
       int ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
       while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
       while (ti * (ti + 1) / 2 > t) --ti;
@@ -138,7 +159,11 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
     return;
   }
 
-  auto tile_of = [&](int i, int& ti, int& tj) { lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj); };
+  int part_dummy;
+  auto tile_of = [&](int i, int& ti, int& tj) {
+    if (own_tab) owned_tile(own_tab, blockIdx.x + i * gridDim.x, ti, tj, part_dummy);
+    else lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj);
+  };
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -177,8 +202,9 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
 
   int q = 0;
   for (int i = 0; i < my_tiles; ++i) {
-    int ti, tj;
-    tile_of(i, ti, tj);
+    int ti, tj, part = 0;
+    if (own_tab) owned_tile(own_tab, blockIdx.x + i * gridDim.x, ti, tj, part);
+    else lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj);
     // warm L2 with this tile's C columns (read-modify-written in the epilogue)
     if (tid < kTile) {
       const int col = tj * kTile + tid;
@@ -226,7 +252,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
       }
     }
 
-    if (bulk_ok && ti > tj) {
+    if (bulk_ok && ti > tj && !part) {
       // warp-local: the warp's boxes are private, so no CTA barrier; lane 0
       // issued this warp's previous reduces and waits for them to drain
       bulk_wait_read0();
@@ -258,6 +284,8 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
 
     const int row_base = ti * kTile + wm * 64 + (lane >> 2);
     const int col_base = tj * kTile + wn * 32 + 2 * (lane & 3);
+    // straddling tile of the column-owned launch: columns of other ranks stay untouched
+    auto mine = [&](int col) { return !part || int(((own_cbase + col) / own_nbd) % own_g) == own_rank; };
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // epilogue in two halves to bound register use
       double cin[4][4][2];
@@ -269,7 +297,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
           for (int e = 0; e < 2; ++e) {
             const int row = row_base + (h * 4 + mm) * 8, col = col_base + ni * 8 + e;
             cin[mm][ni][e] =
-                (beta != 0.0 && row < n && col < n && row > col) ? C[(long long)col * ldc + row] : 0.0;
+                (beta != 0.0 && row < n && col < n && row > col && mine(col)) ? C[(long long)col * ldc + row] : 0.0;
           }
 #pragma unroll
       for (int mm = 0; mm < 4; ++mm)
@@ -278,7 +306,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int row = row_base + (h * 4 + mm) * 8, col = col_base + ni * 8 + e;
-            if (row < n && col < n && row > col)
+            if (row < n && col < n && row > col && mine(col))
               C[(long long)col * ldc + row] =
                   (beta == 1.0 ? cin[mm][ni][e] : beta * cin[mm][ni][e]) + acc[h * 4 + mm][ni][e];
           }
@@ -456,7 +484,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }  // namespace
 
 cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
-                              double* C, long long ldc, int n, double beta, cudaStream_t stream) {
+                              double* C, long long ldc, int n, double beta, cudaStream_t stream,
+                              const ColOwner* own) {
   if (n < 2) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -486,11 +515,37 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   int nt = tiles_for(n);
-  int ntiles = nt * (nt + 1) / 2;
+  int ntiles = own ? own->ntiles : nt * (nt + 1) / 2;
+  if (ntiles == 0) return cudaSuccess;
   int grid = ntiles < nsm ? ntiles : nsm;
-  gemm_lower_nt_kernel<<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc,
-                                                                  n, beta);
+  gemm_lower_nt_kernel<<<grid, kGemmThreads, kGemmSmem, stream>>>(
+      cmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own ? own->tab : nullptr, own ? own->cbase : 0,
+      own ? own->nbd : 1, own ? own->G : 1, own ? own->rank : 0);
   return cudaGetLastError();
+}
+
+int build_owner_table(int n, long long cbase, int nbd, int G, int rank, int* tab) {
+  const int nt = tiles_for(n);
+  int m = 0, total = 0;
+  for (int tj = 0; tj < nt; ++tj) {
+    const long long c0 = cbase + (long long)tj * kTile, c1 = std::min(cbase + n, c0 + kTile);
+    int owned = 0;
+    for (long long c = c0; c < c1;) {  // walk the distribution blocks the tile column crosses
+      const long long bend = std::min(c1, (c / nbd + 1) * nbd);
+      if ((c / nbd) % G == rank) owned += int(bend - c);
+      c = bend;
+    }
+    if (owned == 0) continue;
+    int* e = tab + 2 + 3 * m;
+    e[0] = tj;
+    e[1] = total;
+    e[2] = owned < int(c1 - c0) ? 1 : 0;
+    total += nt - tj;
+    ++m;
+  }
+  tab[0] = m;
+  tab[1] = total;
+  return total;
 }
 
 cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, const double* tau_base,
