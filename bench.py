@@ -10,9 +10,12 @@ Metric: LTL^T factorization GFLOP/s with the reference's n^3/3 flop model
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Multi-GPU: one matrix does not shard across GPUs on this path (DESIGN.md,
-"replicas only"), so N ranks factor N independent matrices (weak scaling);
-value = all ranks' flops / max-over-ranks device time.
+Multi-GPU: the headline config-2 matrix is too small to shard, so N ranks
+factor N independent matrices (weak scaling); value = all ranks' flops /
+max-over-ranks device time.  Under torchrun (N > 1) the line also carries
+config 5 (n=49152) factored ACROSS the N ranks by the block-cyclic driver
+(other_configs.config5_dist_n49152_nb512, strong scaling, device time max over
+ranks); at N = 1 config 5 runs through the single-device driver.
 """
 
 from __future__ import annotations
@@ -190,7 +193,76 @@ def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush):
                                                    "gflops": round(8192 * 256 ** 3 / 3 / (ms * 1e-3) / 1e9, 1),
                                                    "pfaffians_per_s": round(8192 / (ms * 1e-3), 0)}
         del xd
+    torch.cuda.empty_cache()
+    # config 5 on one GPU (the distributed driver runs under torchrun, N > 1)
+    res["config5_blk_piv_n49152_nb512"] = config5_single(torch, pk, dv, fp64_peak, e0, e1)
     return res
+
+
+N5, NB5 = 49152, 512
+FLOPS5 = N5 ** 3 / 3.0
+
+
+def config5_input(torch, n=N5, seed=0):
+    """Config 5 input on the device: X = G - G^T, G iid N(0, 1/n) (torch's CUDA
+    Philox generator, seed 0 -- the same matrix on every rank).  Parity at this
+    size is property-based (tools/run_cfg5.py: residual, log|Pf| = slogdet/2),
+    so the bench skips the 35 s host Philox draw."""
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(seed)
+    G = torch.randn((n, n), generator=gen, dtype=torch.float64, device="cuda")
+    G /= n ** 0.5
+    X = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
+    for j0 in range(0, n, 4096):
+        X[:, j0:j0 + 4096] = G[:, j0:j0 + 4096] - G[j0:j0 + 4096, :].t()
+    del G
+    torch.cuda.empty_cache()
+    return X
+
+
+def config5_single(torch, pk, dv, fp64_peak, e0, e1):
+    """Config 5 (n=49152, nb=512) on ONE GPU through the single-device driver."""
+    X = config5_input(torch)
+    L = dv.empty_colmajor(N5, N5, torch.float64)
+    t5 = torch.empty(N5 - 1, dtype=torch.float64, device="cuda")
+    p5 = torch.empty(N5, dtype=torch.int64, device="cuda")
+    pk.ltlt_blk_piv_device(X, NB5, "var1", out=(L, t5, p5))
+    ms = _time(torch, lambda: pk.ltlt_blk_piv_device(X, NB5, "var1", out=(L, t5, p5)), 2, e0, e1)
+    g5 = FLOPS5 / (ms * 1e-3) / 1e9
+    del X, L
+    dv._WS.clear()
+    torch.cuda.empty_cache()
+    return {"ms": round(ms, 1), "gflops": round(g5, 1), "pct_fp64_peak": round(100 * g5 / 1e3 / fp64_peak, 2),
+            "input": "X=G-G^T, G~N(0,1/n) torch CUDA generator seed 0 (device-generated)"}
+
+
+def config5_distributed(torch, world, rank, fp64_peak):
+    """Config 5 over the N ranks: block-cyclic columns (nbd=512), VMM-mapped peer
+    blocks, NCCL stream barrier (skl_ltlt_blk_piv_dist).  Device time, max over ranks."""
+    from paper_2411_09859_b200.dist import DistLTLT
+    X = config5_input(torch)
+    ctx = DistLTLT(N5, NB5, "var1", nbd=512, barrier="nccl")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for it in range(2):
+        ctx.load_input(X)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0.record()
+        ctx.factorize()
+        e1.record()
+        torch.cuda.synchronize()
+        if it:
+            times.append(e0.elapsed_time(e1))
+    piv = ctx.piv_view().cpu().numpy()
+    ms = max_over_ranks(world, min(times))
+    ctx.close()
+    del X
+    torch.cuda.empty_cache()
+    g = FLOPS5 / (ms * 1e-3) / 1e9
+    return {"ms": round(ms, 1), "gflops": round(g, 1), "ranks": world, "nbd": 512,
+            "pct_fp64_peak_aggregate": round(100 * g / 1e3 / (fp64_peak * world), 2),
+            "nontrivial_pivots": int(np.count_nonzero(piv)), "scaling": "strong (one matrix)"}
 
 
 def cpu_baseline_port(x, budget_s=30.0):
@@ -439,6 +511,24 @@ def main():
         val, reps, dt = cpu_baseline_port(x)
         line["cpu_baseline"] = {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
                                 "sample": f"{reps} full factorization of config 2 by the oracle port ({dt:.1f} s)"}
+    if world > 1 and not args.skip_other:
+        # config 5 across the ranks; a watchdog prints the line without it if the
+        # distributed run does not finish (never leave the driver's run hanging)
+        def watchdog():
+            if rank == 0:
+                line["other_configs"]["config5_dist_n49152_nb512"] = {"error": "timeout (600 s)"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+        timer = threading.Timer(600.0, watchdog)
+        timer.daemon = True
+        timer.start()
+        try:
+            del flush
+            torch.cuda.empty_cache()
+            line["other_configs"]["config5_dist_n49152_nb512"] = config5_distributed(torch, world, rank, fp64_peak)
+        except Exception as exc:  # noqa: BLE001 -- reported in the line
+            line["other_configs"]["config5_dist_n49152_nb512"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        timer.cancel()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -93,20 +93,19 @@ __host__ __device__ __forceinline__ void lower_tile_swizzled(int t, int nt, int&
 
 // Column-owned subset of the lower tiles (block-cyclic multi-GPU driver): tab =
 // [m, total, (tcol, first, partial) x m] lists the tile columns holding at least
-// one column this rank owns; tile t maps to column c with first[c] <= t <
-// first[c+1] and row tj + (t - first[c]).  `partial` tiles straddle a
+// one column this rank owns; tile t maps to entry c with first[c] <= t <
+// first[c+1], tile column tcol[c] and row tcol[c] + (t - first[c]).  `partial` tiles straddle a
 // distribution-block boundary and take the column-masked register epilogue.
-__device__ __forceinline__ void owned_tile(const int* __restrict__ tab, int t, int& ti, int& tj, int& part) {
+// The CTA's tiles t = blockIdx.x + i*gridDim.x ascend, so each walker (producer
+// and consumers) keeps its own column cursor c and only moves it forward: no
+// dependent binary-search loads on the producer's critical path.
+__device__ __forceinline__ void owned_tile(const int* __restrict__ tab, int t, int& c, int& ti, int& tj, int& part) {
   const int m = tab[0];
   const int* e = tab + 2;
-  int lo = 0, hi = m - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (e[3 * mid + 1] <= t) lo = mid; else hi = mid - 1;
-  }
-  tj = e[3 * lo];
-  ti = tj + (t - e[3 * lo + 1]);
-  part = e[3 * lo + 2];
+  while (c + 1 < m && __ldg(e + 3 * (c + 1) + 1) <= t) ++c;
+  tj = __ldg(e + 3 * c);
+  ti = tj + (t - __ldg(e + 3 * c + 1));
+  part = __ldg(e + 3 * c + 2);
 }
 
 // Persistent lower-triangular DGEMM-NT: one CTA per SM walks the lower tiles
@@ -114,6 +113,7 @@ __device__ __forceinline__ void owned_tile(const int* __restrict__ tab, int t, i
 // boundaries so the next tile's operands stream in during the epilogue.  The
 // C tile is prefetched into L2 when a tile starts and read-modified-written
 // in the epilogue (accumulators start at zero).
+template <bool kOwned>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, const double* __restrict__ P,
                      const double* __restrict__ Q, int k4cap, int nk4_host,
@@ -133,7 +133,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
   // the next tile's MMAs; diagonal tiles keep the masked register epilogue
   const bool bulk_ok = use_tmap && beta == 1.0;
   const int nt = tiles_for(n);
-  const int ntiles = own_tab ? own_tab[1] : nt * (nt + 1) / 2;
+  const int ntiles = kOwned ? own_tab[1] : nt * (nt + 1) / 2;
   const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
   const int nchunks = (nk4 + kK4PerStage - 1) / kK4PerStage;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -143,7 +143,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
   if (my_tiles == 0 || nchunks == 0) {
     // nothing to multiply: still apply beta to the owned tiles (the column-owned
     // launches always carry K >= 1)
-    for (int t = blockIdx.x; t < ntiles && nchunks == 0 && !own_tab; t += gridDim.x) {
+    for (int t = blockIdx.x; t < ntiles && nchunks == 0 && !kOwned; t += gridDim.x) {
       int ti = int((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
       while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
       while (ti * (ti + 1) / 2 > t) --ti;
@@ -159,9 +159,9 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
     return;
   }
 
-  int part_dummy;
+  int part_dummy, cur_iss = 0, cur_mma = 0;
   auto tile_of = [&](int i, int& ti, int& tj) {
-    if (own_tab) owned_tile(own_tab, blockIdx.x + i * gridDim.x, ti, tj, part_dummy);
+    if constexpr (kOwned) owned_tile(own_tab, blockIdx.x + i * gridDim.x, cur_iss, ti, tj, part_dummy);
     else lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj);
   };
   if (tid == 0) {
@@ -203,7 +203,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
   int q = 0;
   for (int i = 0; i < my_tiles; ++i) {
     int ti, tj, part = 0;
-    if (own_tab) owned_tile(own_tab, blockIdx.x + i * gridDim.x, ti, tj, part);
+    if constexpr (kOwned) owned_tile(own_tab, blockIdx.x + i * gridDim.x, cur_mma, ti, tj, part);
     else lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj);
     // warm L2 with this tile's C columns (read-modify-written in the epilogue)
     if (tid < kTile) {
@@ -285,7 +285,10 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
     const int row_base = ti * kTile + wm * 64 + (lane >> 2);
     const int col_base = tj * kTile + wn * 32 + 2 * (lane & 3);
     // straddling tile of the column-owned launch: columns of other ranks stay untouched
-    auto mine = [&](int col) { return !part || int(((own_cbase + col) / own_nbd) % own_g) == own_rank; };
+    auto mine = [&](int col) {
+      if constexpr (kOwned) return !part || int(((own_cbase + col) / own_nbd) % own_g) == own_rank;
+      else return true;
+    };
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // epilogue in two halves to bound register use
       double cin[4][4][2];
@@ -489,8 +492,10 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   if (n < 2) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_lower_nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_lower_nt_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kGemmSmem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gemm_lower_nt_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -518,9 +523,13 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   int ntiles = own ? own->ntiles : nt * (nt + 1) / 2;
   if (ntiles == 0) return cudaSuccess;
   int grid = ntiles < nsm ? ntiles : nsm;
-  gemm_lower_nt_kernel<<<grid, kGemmThreads, kGemmSmem, stream>>>(
-      cmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own ? own->tab : nullptr, own ? own->cbase : 0,
-      own ? own->nbd : 1, own ? own->G : 1, own ? own->rank : 0);
+  if (own)
+    gemm_lower_nt_kernel<true><<<grid, kGemmThreads, kGemmSmem, stream>>>(
+        cmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own->tab, own->cbase, own->nbd, own->G, own->rank);
+  else
+    gemm_lower_nt_kernel<false><<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, use_tmap, P, Q, k4cap, nk4,
+                                                                           nk4_dev, C, ldc, n, beta, nullptr, 0, 1,
+                                                                           1, 0);
   return cudaGetLastError();
 }
 

@@ -83,6 +83,9 @@ def main():
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--dist", default="normal_scaled")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--virtual", type=int, default=0,
+                    help="also run the block-cyclic driver over this many virtual ranks and compare")
+    ap.add_argument("--nbd", type=int, default=512)
     a = ap.parse_args()
     n = a.n
     t0 = time.time()
@@ -91,6 +94,9 @@ def main():
     L = dv.empty_colmajor(n, n, torch.float64)
     tau = torch.empty(n - 1, dtype=torch.float64, device="cuda")
     piv = torch.empty(n, dtype=torch.int64, device="cuda")
+    from bench import ClockSampler
+    sampler = ClockSampler(0)
+    sampler.start()
     times = []
     for _ in range(a.reps):
         e0 = torch.cuda.Event(enable_timing=True)
@@ -101,12 +107,46 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
+    clocks = sampler.stop()
+    # per-kernel-class split of one more factorization (CUDA events per launch)
+    import ctypes
+    from paper_2411_09859_b200 import _capi
+    lib = _capi.load()
+    lib.skl_timing_enable(1)
+    pk.ltlt_blk_piv_device(X, a.b, a.fused, out=(L, tau, piv))
+    torch.cuda.synchronize()
+    kms, kcnt = (ctypes.c_double * 4)(), (ctypes.c_int * 4)()
+    lib.skl_timing_read(kms, kcnt)
+    lib.skl_timing_enable(0)
+    split = {k: round(kms[i], 2) for i, k in enumerate(["panel", "pack", "gemm", "finalize"])}
+    split["launches"] = list(kcnt)
     dv._WS.clear()
     torch.cuda.empty_cache()
     ms = min(times)
     flops = n ** 3 / 3
     out = {"n": n, "nb": a.b, "fused": a.fused, "ms": round(ms, 2), "all_ms": [round(t, 2) for t in times],
-           "gflops": round(flops / ms / 1e6, 1), "gen_s": round(gen_s, 1)}
+           "gflops": round(flops / ms / 1e6, 1), "gen_s": round(gen_s, 1), "split_ms": split,
+           "clocks": clocks}
+    if a.virtual:
+        from paper_2411_09859_b200.dist import DistLTLT
+        c = DistLTLT(n, a.b, a.fused, nbd=a.nbd, virtual_ranks=a.virtual)
+        dts = []
+        for _ in range(2):
+            c.load_input(X)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            Ld, taud_, pivd = c.factorize()
+            e1.record()
+            torch.cuda.synchronize()
+            dts.append(e0.elapsed_time(e1))
+        out["virtual"] = {"ranks": a.virtual, "nbd": a.nbd, "ms": round(min(dts), 2),
+                          "piv_equal": bool(torch.equal(pivd, piv)), "tau_equal": bool(torch.equal(taud_, tau)),
+                          "l_equal": bool(torch.equal(torch.tril(Ld, -1), torch.tril(L, -1)))}
+        del Ld, taud_, pivd
+        c.close()
+        torch.cuda.empty_cache()
     if not a.no_check:
         pv = piv.cpu().numpy()
         tv = tau.cpu().numpy()
