@@ -563,15 +563,18 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
       const int ka = rt - p.lo;
       const int K = ka + (straggler ? 2 : 0);
       const int nk4 = (K + 3) / 4;
+      const int sh0 = skl::align_shift(rt, ld), rt0 = rt - sh0;
       {
         KScope ks(KPACK, st);
         SKL_TRY(skl::launch_pack_rankk(ws.W + (size_t)p.lo * ld + rt, ld, ntr, ka, tau + p.lo + 1, -1.0,
-                                       straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st));
+                                       straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st, sh0));
       }
       {
+        // the C region starts sh0 rows/columns early (zero operand rows there) so
+        // every C tile begins on a 128-byte line
         KScope ks(KGEMM, st);
-        SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, ws.W + (size_t)rt * ld + rt, ld, ntr,
-                                       1.0, st));
+        SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, ws.W + (size_t)rt0 * ld + rt0, ld,
+                                       ntr + sh0, 1.0, st));
       }
     }
   }
@@ -735,8 +738,9 @@ int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int r
   for (int k = 0; k < np; ++k) {
     const int rt = plan[k].r + plan[k].nelim;
     if (n - rt < 2) continue;
+    const int rt0 = rt - skl::align_shift(rt, ldw);  // the GEMM's (line-aligned) region origin
     for (int q = 0; q < nr; ++q)
-      ntiles[(size_t)k * nr + q] = skl::build_owner_table(n - rt, rt, nbd, nranks, rank_lo + q,
+      ntiles[(size_t)k * nr + q] = skl::build_owner_table(n - rt0, rt0, nbd, nranks, rank_lo + q,
                                                           tabs.data() + ((size_t)k * nr + q) * dw.tab_stride);
   }
   SKL_TRY(cudaMemcpyAsync(ws.col_group, group.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
@@ -803,19 +807,20 @@ int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int r
       const int ka = rt - p.lo;
       const int K = ka + (straggler ? 2 : 0);
       const int nk4 = (K + 3) / 4;
+      const int sh0 = skl::align_shift(rt, ldw), rt0 = rt - sh0;
       {
         KScope ks(KPACK, st);
         SKL_TRY(skl::launch_pack_rankk(W + (size_t)p.lo * ldw + rt, ldw, ntr, ka, sh.tau + p.lo + 1, -1.0,
-                                       straggler ? sh.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st));
+                                       straggler ? sh.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st, sh0));
       }
       for (int q = 0; q < nr; ++q) {
         const int nt = ntiles[(size_t)k * nr + q];
         if (nt == 0) continue;
-        skl::ColOwner own{dw.own_tab + ((size_t)k * nr + q) * dw.tab_stride, nt, (long long)rt, nbd, nranks,
+        skl::ColOwner own{dw.own_tab + ((size_t)k * nr + q) * dw.tab_stride, nt, (long long)rt0, nbd, nranks,
                           rank_lo + q};
         KScope ks(KGEMM, st);
-        SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, W + (size_t)rt * ldw + rt, ldw, ntr, 1.0,
-                                       st, &own));
+        SKL_TRY(skl::launch_gemm_lower(ws.P, ws.Q, ws.k4cap, nk4, nullptr, W + (size_t)rt0 * ldw + rt0, ldw,
+                                       ntr + sh0, 1.0, st, &own));
       }
       if ((rc = sync())) return rc;
     }

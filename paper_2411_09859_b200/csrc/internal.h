@@ -38,10 +38,16 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
                               const ColOwner* own = nullptr);
 
 // P = alpha*A, Q = A T^T with T tridiag(t) (t = tau_base[0..ka-2]); optional
-// var1 straggler columns (l = A[:, ka-1], y) zeroed on row 0.
+// var1 straggler columns (l = A[:, ka-1], y) zeroed on row 0.  shift > 0
+// prepends that many zero rows (P, Q then hold rows + shift rows).
 cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, const double* tau_base,
                               double alpha, const double* y, int k4cap, double* P, double* Q,
-                              cudaStream_t stream);
+                              cudaStream_t stream, int shift = 0);
+
+// rows/columns of zero padding that put the trailing C region [rt:, rt:] of a
+// column-major matrix with leading dimension ld on 128-byte lines (TMA boxes
+// and L2 lines then never straddle); 0 when ld is not a multiple of 16
+inline int align_shift(int rt, long long ld) { return (ld % 16 == 0) ? (rt & 15) : 0; }
 
 // skr2k: keep[] (device) lists columns nonzero in both A and B; count at keff_dev.
 cudaError_t launch_rank2k_keep(const double* A, long long lda, const double* B, long long ldb, int n, int k,

@@ -115,7 +115,8 @@ __device__ __forceinline__ void owned_tile(const int* __restrict__ tab, int t, i
 // in the epilogue (accumulators start at zero).
 template <bool kOwned>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, const double* __restrict__ P,
+gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_constant__ CUtensorMap pmap, int use_tmap,
+                     const double* __restrict__ P,
                      const double* __restrict__ Q, int k4cap, int nk4_host,
                      const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta,
                      const int* __restrict__ own_tab, long long own_cbase, int own_nbd, int own_g, int own_rank) {
@@ -205,8 +206,22 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, int use_tmap, con
     int ti, tj, part = 0;
     if constexpr (kOwned) owned_tile(own_tab, blockIdx.x + i * gridDim.x, cur_mma, ti, tj, part);
     else lower_tile_swizzled(blockIdx.x + i * gridDim.x, nt, ti, tj);
-    // warm L2 with this tile's C columns (read-modify-written in the epilogue)
-    if (tid < kTile) {
+    // warm L2 with the NEXT tile's C block (read-modify-written in its
+    // epilogue): one 128x128 tensor prefetch issued a whole tile ahead by a
+    // thread that is not the operand producer
+    if (tid == 32 && use_tmap) {
+      if (i == 0) prefetch_l2_tensor_2d(&pmap, ti * kTile, tj * kTile);
+      if (i + 1 < my_tiles) {
+        int nti, ntj, npart;
+        if constexpr (kOwned) {
+          int cur_pf = cur_mma;
+          owned_tile(own_tab, blockIdx.x + (i + 1) * gridDim.x, cur_pf, nti, ntj, npart);
+        } else {
+          lower_tile_swizzled(blockIdx.x + (i + 1) * gridDim.x, nt, nti, ntj);
+        }
+        prefetch_l2_tensor_2d(&pmap, nti * kTile, ntj * kTile);
+      }
+    } else if (!use_tmap && tid < kTile) {
       const int col = tj * kTile + tid;
       const int r0 = ti * kTile;
       if (col < n && r0 < n) {
@@ -332,16 +347,19 @@ __device__ __forceinline__ void packed_decode(size_t off, int k4cap, int& row, i
 // optional var1 straggler pair (rows >= 1 only; l = A[:, ka-1]):
 //   P[:, ka] = l,  P[:, ka+1] = -y,  Q[:, ka] = y,  Q[:, ka+1] = l
 // so that sum_k P Q^T = alpha A T A^T + l y^T - y l^T.
+// shift > 0: packed rows [0, shift) are zero and packed row r holds A row
+// r - shift (the driver aligns the C region to 128-byte lines that way)
 __global__ void pack_rankk_kernel(const double* __restrict__ A, long long lda, int rows, int ka,
                                   const double* __restrict__ t, double alpha, const double* __restrict__ y,
-                                  int k4cap, double* __restrict__ P, double* __restrict__ Q) {
-  const size_t total = (size_t)tiles_for(rows) * kTile * 4 * k4cap;
+                                  int k4cap, double* __restrict__ P, double* __restrict__ Q, int shift) {
+  const size_t total = (size_t)tiles_for(rows + shift) * kTile * 4 * k4cap;
   for (size_t off = blockIdx.x * (size_t)blockDim.x + threadIdx.x; off < total;
        off += (size_t)gridDim.x * blockDim.x) {
     int row, col;
     packed_decode(off, k4cap, row, col);
+    row -= shift;
     double p = 0.0, q = 0.0;
-    if (row < rows) {
+    if (row >= 0 && row < rows) {
       if (col < ka) {
         const double* ar = A + row;
         p = alpha * ar[(long long)col * lda];
@@ -507,8 +525,9 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   }
   // tensor map over C (rows x cols = n x n, column stride ldc) for the
   // bulk-reduce epilogue; needs a 16-byte aligned base and an even ldc
-  CUtensorMap cmap;
+  CUtensorMap cmap, pmap;
   memset(&cmap, 0, sizeof(cmap));
+  memset(&pmap, 0, sizeof(pmap));
   int use_tmap = 0;
   PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
   if (enc && beta == 1.0 && (ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
@@ -518,6 +537,12 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
     use_tmap = enc(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    // L2 prefetch map: one 128 x 128 box per C tile (no swizzle; prefetch only)
+    cuuint32_t pbox[2] = {(cuuint32_t)kTile, (cuuint32_t)kTile};
+    use_tmap = use_tmap &&
+               enc(&pmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, C, dims, strides, pbox, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   int nt = tiles_for(n);
   int ntiles = own ? own->ntiles : nt * (nt + 1) / 2;
@@ -525,9 +550,10 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   int grid = ntiles < nsm ? ntiles : nsm;
   if (own)
     gemm_lower_nt_kernel<true><<<grid, kGemmThreads, kGemmSmem, stream>>>(
-        cmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own->tab, own->cbase, own->nbd, own->G, own->rank);
+        cmap, pmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own->tab, own->cbase, own->nbd, own->G,
+        own->rank);
   else
-    gemm_lower_nt_kernel<false><<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, use_tmap, P, Q, k4cap, nk4,
+    gemm_lower_nt_kernel<false><<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, pmap, use_tmap, P, Q, k4cap, nk4,
                                                                            nk4_dev, C, ldc, n, beta, nullptr, 0, 1,
                                                                            1, 0);
   return cudaGetLastError();
@@ -559,9 +585,10 @@ int build_owner_table(int n, long long cbase, int nbd, int G, int rank, int* tab
 
 cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, const double* tau_base,
                               double alpha, const double* y, int k4cap, double* P, double* Q,
-                              cudaStream_t stream) {
-  size_t total = packed_elems(rows, k4cap);
-  pack_rankk_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, rows, ka, tau_base, alpha, y, k4cap, P, Q);
+                              cudaStream_t stream, int shift) {
+  size_t total = packed_elems(rows + shift, k4cap);
+  pack_rankk_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, rows, ka, tau_base, alpha, y, k4cap, P, Q,
+                                                              shift);
   return cudaGetLastError();
 }
 
