@@ -145,14 +145,21 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
     }
   }
   static int multi = env_int("SKL_MULTI_CLUSTER", 1);
+  static int multi_q = env_int("SKL_MULTI_Q", 0);    // cap on the co-resident clusters used
+  // cap on the multi-cluster panel width: n=16384 sweep (tools/sweep_multi.sh) 117.8-118.6 ms at 128
+  // vs 120.7 ms uncapped (256): the per-step gemv grows with the width faster than the GEMM gains
+  static int multi_nb = env_int("SKL_MULTI_NB", 128);
   if (Cmax > 0 && multi) {
     for (int csize : {Cmax, 8}) {
-      const int Q = skl::panel_multi_clusters(csize, smem_limit());
+      int Q = skl::panel_multi_clusters(csize, smem_limit());
+      if (multi_q > 0 && Q > multi_q) {
+        Q = std::max(multi_q, 2);
+      }
       if (Q < 2) continue;
       const int P = Q * csize;
       const int Rm = (rows + P - 1) / P;
       if (Rm > 512) continue;
-      int w = want;
+      int w = (multi_nb > 0 && want > multi_nb) ? multi_nb : want;
       while (w >= 1 && skl::panel_cluster_smem_bytes(Rm, r + w - lo) > smem_limit()) --w;
       if (w >= 1 && w >= std::min(want, 64)) {
         p = PanelPlan{r, w, lo, P, Rm, r + w - lo, 2, csize};
