@@ -56,6 +56,16 @@ int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, 
 
 /* skew_tridiag_rankk (kernels3.py:151-209):
  *   C_lower := beta*C + alpha * A T A^T, T = tridiag(tau[0..k-2]) skew.     */
+/* skew_tridiag_gemm (kernels3.py:239-302): C (p x q) := beta*C + alpha*A (T B)
+ *   with A (p x k), B (k x q), T = tridiag(tau) skew (T[i+1,i] = tau_i,
+ *   T[i,i+1] = -tau_i).  tril != 0 writes only the entries with row > col
+ *   (the trapezoidal from-the-left update of ltlt_blk_left, blocked.py:236-265);
+ *   otherwise every entry.  C must not alias A or B (SKL_ALIAS).            */
+size_t skl_skew_tridiag_gemm_workspace_size(int p, int q, int k);
+int skl_skew_tridiag_gemm(int p, int q, int k, double alpha, const double* A, long long lda, const double* tau,
+                          const double* B, long long ldb, double beta, double* C, long long ldc, int tril,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 size_t skl_sktri_rankk_workspace_size(int n, int k);
 int skl_sktri_rankk_lower(int n, int k, double alpha, const double* A, long long lda, const double* tau,
                           double beta, double* C, long long ldc, void* workspace, size_t workspace_bytes,
@@ -199,8 +209,8 @@ int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int r
                           size_t workspace_bytes, skl_barrier_fn barrier, void* barrier_ctx, void* stream);
 /* host only: owned-tile table of the column-filtered trailing GEMM (the lower
  *   triangle of an n x n region whose column 0 is global column cbase):
- *   tab = [m, total, (tile column, first tile, partial) x m]; tab_ints >=
- *   2 + 3*ceil(n/128).                                                        */
+ *   tab = [m, total, (tile column, first tile, partial, first tile row) x m];
+ *   tab_ints >= 2 + 4*ceil(n/128).                                                       */
 int skl_dist_owner_table(int n, long long cbase, int nbd, int nranks, int rank, int* tab, size_t tab_ints);
 
 /* CUDA VMM plumbing (driver API through cudaGetDriverEntryPoint): physical

@@ -372,6 +372,48 @@ int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, 
   return SKL_OK;
 }
 
+// skew_tridiag_gemm (kernels3.py:239-302): C (p x q) := beta C + alpha A (T B);
+// tril: only row > col of the view.  The same DMMA kernel in tile-table mode.
+size_t skl_skew_tridiag_gemm_workspace_size(int p, int q, int k) {
+  Bump b(nullptr);
+  const int k4cap = (std::max(k, 1) + 3) / 4;
+  b.take<double>(skl::packed_elems(std::max(p, 1), k4cap));
+  b.take<double>(skl::packed_elems(std::max(q, 1), k4cap));
+  b.take<int>(skl::owner_table_ints(std::max(q, 1)));
+  return b.off + 256;
+}
+
+int skl_skew_tridiag_gemm(int p, int q, int k, double alpha, const double* A, long long lda, const double* tau,
+                          const double* B, long long ldb, double beta, double* C, long long ldc, int tril,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (p < 0 || q < 0 || k < 0 || (p > 0 && ldc < p) || (p > 0 && k > 0 && lda < p) || (q > 0 && k > 0 && ldb < k))
+    return SKL_BAD_ARGUMENT;
+  if (workspace_bytes < skl_skew_tridiag_gemm_workspace_size(p, q, k)) return SKL_BAD_ARGUMENT;
+  if (k > 0 && overlaps(C, mat_bytes(p, q, ldc), A, mat_bytes(p, k, lda))) return SKL_ALIAS;
+  if (k > 0 && overlaps(C, mat_bytes(p, q, ldc), B, mat_bytes(k, q, ldb))) return SKL_ALIAS;
+  if (p == 0 || q == 0) return SKL_OK;
+  if (alpha == 0.0 || k == 0) {
+    g_kt.launches += beta != 1.0 ? 1 : 0;
+    SKL_TRY(skl::launch_scale_block(C, ldc, p, q, beta, tril ? 1 : 0, st));
+    return SKL_OK;
+  }
+  Bump b(workspace);
+  const int k4cap = (k + 3) / 4;
+  double* P = b.take<double>(skl::packed_elems(p, k4cap));
+  double* Q = b.take<double>(skl::packed_elems(q, k4cap));
+  int* tab_dev = b.take<int>(skl::owner_table_ints(q));
+  std::vector<int> tab(skl::owner_table_ints(q), 0);
+  const int ntiles = skl::build_rect_table(p, q, tril ? 1 : 0, tab.data());
+  if (ntiles == 0) return SKL_OK;  // tril with q >= p... nothing strictly below the diagonal
+  SKL_TRY(cudaMemcpyAsync(tab_dev, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, st));
+  g_kt.launches += 2;
+  SKL_TRY(skl::launch_pack_gemm(A, lda, p, B, ldb, q, k, tau, alpha, k4cap, P, Q, st));
+  skl::ColOwner own{tab_dev, ntiles, 0, 1 << 30, 1, 0};
+  SKL_TRY(skl::launch_gemm_lower(P, Q, k4cap, k4cap, nullptr, C, ldc, p, beta, st, &own, q, tril ? 1 : 0));
+  return SKL_OK;
+}
+
 size_t skl_sktri_rankk_workspace_size(int n, int k) {
   Bump b(nullptr);
   int k4cap = (std::max(k, 1) + 3) / 4;

@@ -28,14 +28,25 @@ struct ColOwner {
 // host: owned-tile table for the lower triangle of an n x n region whose column
 // 0 is global column cbase; tab needs 2 + 3*tiles_for(n) ints; returns the tile count
 int build_owner_table(int n, long long cbase, int nbd, int G, int rank, int* tab);
-inline size_t owner_table_ints(int n) { return 2 + 3 * (size_t)tiles_for(n); }
+inline size_t owner_table_ints(int n) { return 2 + 4 * (size_t)tiles_for(n); }
+// host: tile table of a general p x q block (tri = 0) or of its strictly-lower
+// trapezoid (tri = 1) for launch_gemm_lower(..., own, q, tri); tab needs
+// owner_table_ints(q) ints; returns the tile count
+int build_rect_table(int p, int q, int tri, int* tab);
 
 // C[i,j] (i>j, i,j < n) = beta*C[i,j] + sum_k P[i,k] Q[j,k]
 // nk4_dev (optional) overrides nk4 with a device-resident count; own (optional)
 // restricts the update to one rank's columns.
 cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
                               double* C, long long ldc, int n, double beta, cudaStream_t stream,
-                              const ColOwner* own = nullptr);
+                              const ColOwner* own = nullptr, int ncols = -1, int tri = 1);
+
+// skew_tridiag_gemm operands: P = alpha*A (p x k), Q = (T B)^T (q x k) with
+// B (k x q, column stride ldb) and T tridiag(t): Q[j,c] = t[c-1] B[c-1,j] - t[c] B[c+1,j]
+cudaError_t launch_pack_gemm(const double* A, long long lda, int p, const double* B, long long ldb, int q, int k,
+                             const double* t, double alpha, int k4cap, double* P, double* Q, cudaStream_t stream);
+// C (p x q) *= beta on every entry (tri = 0) or on row > col only
+cudaError_t launch_scale_block(double* C, long long ldc, int p, int q, double beta, int tri, cudaStream_t stream);
 
 // P = alpha*A, Q = A T^T with T tridiag(t) (t = tau_base[0..ka-2]); optional
 // var1 straggler columns (l = A[:, ka-1], y) zeroed on row 0.  shift > 0

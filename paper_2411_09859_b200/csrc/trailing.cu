@@ -91,21 +91,24 @@ __host__ __device__ __forceinline__ void lower_tile_swizzled(int t, int nt, int&
   ti = tj + u;
 }
 
-// Column-owned subset of the lower tiles (block-cyclic multi-GPU driver): tab =
-// [m, total, (tcol, first, partial) x m] lists the tile columns holding at least
-// one column this rank owns; tile t maps to entry c with first[c] <= t <
-// first[c+1], tile column tcol[c] and row tcol[c] + (t - first[c]).  `partial` tiles straddle a
-// distribution-block boundary and take the column-masked register epilogue.
+// Tile-table mode (kOwned): tab = [m, total, (tcol, first, partial, row0) x m]
+// lists tile columns; column entry c holds the tiles t with first[c] <= t <
+// first[c+1], tile column tcol[c] and rows row0[c] + (t - first[c]).  Used by
+//  * the block-cyclic multi-GPU driver: the lower tiles (row0 = tcol) of the
+//    columns one rank owns; `partial` tiles straddle an owner boundary and take
+//    the column-masked register epilogue;
+//  * skew_tridiag_gemm: a general p x q block (row0 = 0, tri = 0) or its
+//    strictly-lower trapezoid (row0 = tcol, tri = 1).
 // The CTA's tiles t = blockIdx.x + i*gridDim.x ascend, so each walker (producer
 // and consumers) keeps its own column cursor c and only moves it forward: no
 // dependent binary-search loads on the producer's critical path.
 __device__ __forceinline__ void owned_tile(const int* __restrict__ tab, int t, int& c, int& ti, int& tj, int& part) {
   const int m = tab[0];
   const int* e = tab + 2;
-  while (c + 1 < m && __ldg(e + 3 * (c + 1) + 1) <= t) ++c;
-  tj = __ldg(e + 3 * c);
-  ti = tj + (t - __ldg(e + 3 * c + 1));
-  part = __ldg(e + 3 * c + 2);
+  while (c + 1 < m && __ldg(e + 4 * (c + 1) + 1) <= t) ++c;
+  tj = __ldg(e + 4 * c);
+  ti = __ldg(e + 4 * c + 3) + (t - __ldg(e + 4 * c + 1));
+  part = __ldg(e + 4 * c + 2);
 }
 
 // Persistent lower-triangular DGEMM-NT: one CTA per SM walks the lower tiles
@@ -119,7 +122,10 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
                      const double* __restrict__ P,
                      const double* __restrict__ Q, int k4cap, int nk4_host,
                      const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta,
-                     const int* __restrict__ own_tab, long long own_cbase, int own_nbd, int own_g, int own_rank) {
+                     const int* __restrict__ own_tab, long long own_cbase, int own_nbd, int own_g, int own_rank,
+                     int ncols, int tri) {
+  // n: C rows; ncols: C columns (== n and tri == 1 except for the tile-table
+  // rectangular mode of skew_tridiag_gemm); tri: only row > col is written
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // 1 KiB-align the carve-up (the swizzled boxes need it)
   unsigned char* smem_al = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -224,7 +230,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
     } else if (!use_tmap && tid < kTile) {
       const int col = tj * kTile + tid;
       const int r0 = ti * kTile;
-      if (col < n && r0 < n) {
+      if (col < ncols && r0 < n) {
         const int rows = min(kTile, n - r0);
         const double* src = C + (long long)col * ldc + r0;
         uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
@@ -267,7 +273,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
       }
     }
 
-    if (bulk_ok && ti > tj && !part) {
+    if (bulk_ok && !part && (ti > tj || (kOwned && !tri))) {
       // warp-local: the warp's boxes are private, so no CTA barrier; lane 0
       // issued this warp's previous reduces and waits for them to drain
       bulk_wait_read0();
@@ -315,7 +321,9 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
           for (int e = 0; e < 2; ++e) {
             const int row = row_base + (h * 4 + mm) * 8, col = col_base + ni * 8 + e;
             cin[mm][ni][e] =
-                (beta != 0.0 && row < n && col < n && row > col && mine(col)) ? C[(long long)col * ldc + row] : 0.0;
+                (beta != 0.0 && row < n && col < ncols && (row > col || !tri) && mine(col))
+                    ? C[(long long)col * ldc + row]
+                    : 0.0;
           }
 #pragma unroll
       for (int mm = 0; mm < 4; ++mm)
@@ -324,7 +332,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int row = row_base + (h * 4 + mm) * 8, col = col_base + ni * 8 + e;
-            if (row < n && col < n && row > col && mine(col))
+            if (row < n && col < ncols && (row > col || !tri) && mine(col))
               C[(long long)col * ldc + row] =
                   (beta == 1.0 ? cin[mm][ni][e] : beta * cin[mm][ni][e]) + acc[h * 4 + mm][ni][e];
           }
@@ -382,6 +390,38 @@ __global__ void pack_rankk_kernel(const double* __restrict__ A, long long lda, i
     P[off] = p;
     Q[off] = q;
   }
+}
+
+// skew_tridiag_gemm (kernels3.py:239-302): P = alpha*A (p rows), Q = (T B)^T
+// (q rows) with Q[j, c] = t[c-1] B[c-1, j] - t[c] B[c+1, j]
+__global__ void pack_gemm_kernel(const double* __restrict__ A, long long lda, int p, const double* __restrict__ B,
+                                 long long ldb, int q, int k, const double* __restrict__ t, double alpha, int k4cap,
+                                 double* __restrict__ P, double* __restrict__ Q) {
+  const size_t totp = (size_t)tiles_for(p) * kTile * 4 * k4cap, totq = (size_t)tiles_for(q) * kTile * 4 * k4cap;
+  const size_t total = totp > totq ? totp : totq;
+  for (size_t off = blockIdx.x * (size_t)blockDim.x + threadIdx.x; off < total;
+       off += (size_t)gridDim.x * blockDim.x) {
+    int row, col;
+    packed_decode(off, k4cap, row, col);
+    if (off < totp) P[off] = (row < p && col < k) ? alpha * A[(long long)col * lda + row] : 0.0;
+    if (off < totq) {
+      double v = 0.0;
+      if (row < q && col < k) {
+        const double* bj = B + (long long)row * ldb;
+        if (col >= 1) v = t[col - 1] * bj[col - 1];
+        if (col + 1 < k) v -= t[col] * bj[col + 1];
+      }
+      Q[off] = v;
+    }
+  }
+}
+
+__global__ void scale_block_kernel(double* __restrict__ C, long long ldc, int p, int q, double beta, int tri) {
+  for (int j = blockIdx.y; j < q; j += gridDim.y)
+    for (int i = (tri ? j + 1 : 0) + blockIdx.x * blockDim.x + threadIdx.x; i < p; i += gridDim.x * blockDim.x) {
+      double* c = C + (long long)j * ldc + i;
+      *c = beta == 0.0 ? 0.0 : beta * *c;
+    }
 }
 
 // keep[j] = column j is nonzero in both A and B (kernels3.py:318-321);
@@ -506,8 +546,9 @@ PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 
 cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int nk4, const int* nk4_dev,
                               double* C, long long ldc, int n, double beta, cudaStream_t stream,
-                              const ColOwner* own) {
-  if (n < 2) return cudaSuccess;
+                              const ColOwner* own, int ncols, int tri) {
+  if (ncols < 0) ncols = n;
+  if (n < 1 || (own == nullptr && n < 2)) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm_lower_nt_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -531,7 +572,7 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   int use_tmap = 0;
   PFN_cuTensorMapEncodeTiled_v12000 enc = tmap_encoder();
   if (enc && beta == 1.0 && (ldc & 1) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0) {
-    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)ncols};
     cuuint64_t strides[1] = {(cuuint64_t)ldc * sizeof(double)};
     cuuint32_t box[2] = {(cuuint32_t)kBoxRows, (cuuint32_t)kBoxCols}, es[2] = {1, 1};
     use_tmap = enc(&cmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, C, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -551,11 +592,11 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   if (own)
     gemm_lower_nt_kernel<true><<<grid, kGemmThreads, kGemmSmem, stream>>>(
         cmap, pmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own->tab, own->cbase, own->nbd, own->G,
-        own->rank);
+        own->rank, ncols, tri);
   else
     gemm_lower_nt_kernel<false><<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, pmap, use_tmap, P, Q, k4cap, nk4,
                                                                            nk4_dev, C, ldc, n, beta, nullptr, 0, 1,
-                                                                           1, 0);
+                                                                           1, 0, n, 1);
   return cudaGetLastError();
 }
 
@@ -571,11 +612,31 @@ int build_owner_table(int n, long long cbase, int nbd, int G, int rank, int* tab
       c = bend;
     }
     if (owned == 0) continue;
-    int* e = tab + 2 + 3 * m;
+    int* e = tab + 2 + 4 * m;
     e[0] = tj;
     e[1] = total;
     e[2] = owned < int(c1 - c0) ? 1 : 0;
+    e[3] = tj;
     total += nt - tj;
+    ++m;
+  }
+  tab[0] = m;
+  tab[1] = total;
+  return total;
+}
+
+int build_rect_table(int p, int q, int tri, int* tab) {
+  const int ntr = tiles_for(p), ntc = tiles_for(q);
+  int m = 0, total = 0;
+  for (int tj = 0; tj < ntc; ++tj) {
+    const int row0 = tri ? tj : 0;
+    if (row0 >= ntr) break;
+    int* e = tab + 2 + 4 * m;
+    e[0] = tj;
+    e[1] = total;
+    e[2] = 0;
+    e[3] = row0;
+    total += ntr - row0;
     ++m;
   }
   tab[0] = m;
@@ -589,6 +650,20 @@ cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, 
   size_t total = packed_elems(rows + shift, k4cap);
   pack_rankk_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, rows, ka, tau_base, alpha, y, k4cap, P, Q,
                                                               shift);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_gemm(const double* A, long long lda, int p, const double* B, long long ldb, int q, int k,
+                             const double* t, double alpha, int k4cap, double* P, double* Q, cudaStream_t stream) {
+  const size_t total = std::max(packed_elems(p, k4cap), packed_elems(q, k4cap));
+  pack_gemm_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, p, B, ldb, q, k, t, alpha, k4cap, P, Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_block(double* C, long long ldc, int p, int q, double beta, int tri, cudaStream_t stream) {
+  if (p <= 0 || q <= 0 || beta == 1.0) return cudaSuccess;
+  dim3 grid((p + 255) / 256 < 8 ? (p + 255) / 256 : 8, q < 4096 ? q : 4096);
+  scale_block_kernel<<<grid, 256, 0, stream>>>(C, ldc, p, q, beta, tri);
   return cudaGetLastError();
 }
 

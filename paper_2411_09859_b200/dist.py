@@ -86,10 +86,11 @@ def owner_table(n, cbase, nbd, nranks, rank):
     """The column-filtered GEMM's owned-tile table (skl_dist_owner_table)."""
     lib = _capi.load()
     nt = (n + 127) // 128
-    tab = (C.c_int * (2 + 3 * nt))()
+    tab = (C.c_int * (2 + 4 * nt))()
     _capi.check(lib.skl_dist_owner_table(n, cbase, nbd, nranks, rank, tab, len(tab)), "dist_owner_table")
     m = tab[0]
-    rows = [(tab[2 + 3 * c], tab[3 + 3 * c], tab[4 + 3 * c]) for c in range(m)]
+    rows = [(tab[2 + 4 * c], tab[3 + 4 * c], tab[4 + 4 * c]) for c in range(m)]
+    assert all(tab[5 + 4 * c] == tab[2 + 4 * c] for c in range(m))  # lower tiles: rows start at the diagonal
     return tab[1], rows
 
 

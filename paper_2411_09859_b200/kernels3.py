@@ -2,7 +2,8 @@
 
 Same signatures and in-place semantics as the reference:
 ``skew_rank2k`` (kernels3.py:305-351), ``skew_tridiag_rankk``
-(kernels3.py:151-209), ``form_w`` (kernels3.py:354-364).  Operands may be
+(kernels3.py:151-209), ``skew_tridiag_gemm`` (kernels3.py:239-302),
+``form_w`` (kernels3.py:354-364).  Operands may be
 NumPy arrays (copied to the GPU and the output view written back) or
 column-major torch CUDA tensors (updated in place on the device).
 """
@@ -79,6 +80,32 @@ def skew_tridiag_rankk(c, alpha, a, t: SkewTridiagonal, beta=1, *, fused=True, w
     return None
 
 
+def skew_tridiag_gemm(c, alpha, a, t: SkewTridiagonal, b, beta=1, *, tril=False, fused=True, workers=None):
+    """C := beta*C + alpha * A (T B) on a general p x q block (kernels3.py:239-302);
+    ``tril=True`` writes only the entries with row > col.  ``fused`` and
+    ``workers`` are accepted for signature compatibility: T B is always formed
+    inside the operand pack (the fused form) and the CUDA grid replaces the pool."""
+    p, k = a.shape
+    kb, q = b.shape
+    if kb != k or tuple(c.shape) != (p, q) or t.m != k:
+        raise ValueError("dimension mismatch")
+    _check_alias(c, a, "a")
+    _check_alias(c, b, "b")
+    tt = dv.require_cuda()
+    cd, ad, bd = _dev(c), _dev(a), _dev(b)
+    tau = t.tau if _is_torch(t.tau) else dv.vec_to_device(np.asarray(t.tau, dtype=np.float64), tt.float64)
+    lib = _capi.load()
+    nbytes = lib.skl_skew_tridiag_gemm_workspace_size(p, q, k)
+    ws = dv.workspace(nbytes)
+    st = lib.skl_skew_tridiag_gemm(p, q, k, float(alpha), ad.data_ptr() if ad.numel() else None, dv.ld_of(ad),
+                                   tau.data_ptr() if tau.numel() else None, bd.data_ptr() if bd.numel() else None,
+                                   dv.ld_of(bd), float(beta), cd.data_ptr(), dv.ld_of(cd), 1 if tril else 0,
+                                   ws.data_ptr(), nbytes, dv.stream_ptr())
+    _capi.check(st, "skew_tridiag_gemm")
+    _writeback(c, cd)
+    return None
+
+
 def form_w(a, s):
     """W = A S (every other column zero, starting with the first)."""
     n, kdim = a.shape
@@ -112,4 +139,4 @@ def form_w_device(a, tau):
     return wd
 
 
-__all__ = ["skew_rank2k", "skew_tridiag_rankk", "form_w", "form_w_device", "SSplitting"]
+__all__ = ["skew_rank2k", "skew_tridiag_rankk", "skew_tridiag_gemm", "form_w", "form_w_device", "SSplitting"]

@@ -17,6 +17,8 @@ Fixtures
   solve_small.npz      apps.solve (SURVEY 8f rank 2): n in {2, 8, 64, 300}, 1 and 3 right-hand sides;
                        SingularT row for odd n
   mm_small.mtx         mmio.mm_write of a 9x9 skew matrix (the Matrix Market format)
+  l3_small.npz         kernels3.skew_tridiag_gemm: general and tril blocks, several
+                       (p, q, k, alpha, beta) incl. p < q, k = 0 and beta = 0: inputs and outputs
   unpiv_small.npz      unpivoted drivers: ltlt_blk_var1/2a/2b/twostep/left x panel
                        variants ll/rl/twostep, ltlt_unb_rl (+pivoted), ltlt_unb_ll (+first_column),
                        ltlt_unb_panel (ll/rl/twostep, pivoted, first_column) at n in {64, 150, 301}:
@@ -40,6 +42,9 @@ sys.path.insert(0, REF)
 sys.path.insert(0, str(HERE.parent.parent))
 
 from paper_2411_09859_b200.inputs import skew_lower  # noqa: E402
+
+sys.path.insert(0, str(HERE))
+from l3_cases import L3_CASES, l3_inputs  # noqa: E402
 
 
 def ref():
@@ -188,6 +193,19 @@ def main():
             put(f"n{n}_panel40_first", sk.ltlt_unb_panel(X, 40, first_column=fcv), n)
         np.savez_compressed(HERE / "unpiv_small.npz", **d)
         print("unpiv ok", flush=True)
+    if want("l3"):
+        d = {}
+        # inputs are regenerated by the tests from Philox(1000 + i) in the order a, b, tau, c
+        for i, (p_, q_, k_, tril, alpha, beta) in enumerate(L3_CASES):
+            a, b, tau, c = l3_inputs(i, p_, q_, k_)
+            out = c.copy(order="F")
+            sk.kernels3.skew_tridiag_gemm(out, alpha, a, sk.SkewTridiagonal(tau), b, beta, tril=tril)
+            d[f"c{i}_meta"] = np.array([p_, q_, k_, int(tril), alpha, beta])
+            d[f"c{i}_out"] = out
+        cases = L3_CASES
+        d["ncases"] = np.array(len(cases))
+        np.savez_compressed(HERE / "l3_small.npz", **d)
+        print("l3 ok", flush=True)
     if want("solve"):
         d = {}
         for n in (2, 8, 64, 300):

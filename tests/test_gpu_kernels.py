@@ -142,3 +142,48 @@ def test_apply_symmetric_pivot_bit_exact():
         assert np.array_equal(sx.data, want)
     with pytest.raises(IndexError):
         apply_symmetric_pivot(SkewMatrixLower(x), 35, 10)
+
+
+@pytest.mark.parametrize("i", range(9))
+def test_skew_tridiag_gemm_vs_reference_fixture(golden, i):
+    """skl_skew_tridiag_gemm (DMMA kernel, tile-table mode) vs the reference's
+    kernels3.skew_tridiag_gemm on general and tril blocks (p < q, beta in
+    {0, 2, -1}, alpha = 0, k up to 150); untouched entries bit-identical."""
+    import sys
+    from conftest import GOLDEN
+    from paper_2411_09859_b200.core import SkewTridiagonal
+    sys.path.insert(0, str(GOLDEN))
+    from l3_cases import L3_CASES, l3_inputs
+    g = golden("l3_small.npz")
+    p, q, k, tril, alpha, beta = L3_CASES[i]
+    a, b, tau, c = l3_inputs(i, p, q, k)
+    want = g[f"c{i}_out"]
+    got = c.copy(order="F")
+    k3().skew_tridiag_gemm(got, alpha, a, SkewTridiagonal(tau), b, beta, tril=tril)
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12 * max(k, 1))
+    if tril:
+        up = ~np.tril(np.ones((p, q), bool), -1)
+        assert np.array_equal(got[up], c[up])
+
+
+def test_skew_tridiag_gemm_device_tensors_and_alias():
+    import torch
+    from paper_2411_09859_b200 import device as dv
+    from paper_2411_09859_b200.core import SkewTridiagonal
+    p, q, k = 700, 300, 96
+    a = RNG.standard_normal((p, k))
+    b = RNG.standard_normal((k, q))
+    tau = RNG.standard_normal(k - 1)
+    c = np.asfortranarray(RNG.standard_normal((p, q)))
+    want = c.copy()
+    oracle.skew_tridiag_gemm(want, -1.0, a, tau, b, tril=True)
+    cd = dv.to_device_colmajor(c)
+    k3().skew_tridiag_gemm(cd, -1.0, dv.to_device_colmajor(a), SkewTridiagonal(torch.as_tensor(tau, device="cuda")),
+                           dv.to_device_colmajor(b), 1.0, tril=True)
+    assert np.allclose(dv.to_host_colmajor(cd), want, rtol=1e-12, atol=1e-12 * k)
+    x = np.asfortranarray(RNG.standard_normal((8, 8)))
+    with pytest.raises(ValueError):
+        k3().skew_tridiag_gemm(x, 1.0, x, SkewTridiagonal(np.ones(7)), np.ones((8, 8)))
+    with pytest.raises(ValueError):
+        k3().skew_tridiag_gemm(np.zeros((5, 4)), 1.0, np.zeros((5, 3)), SkewTridiagonal(np.ones(2)),
+                               np.zeros((3, 5)))

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import EPS, lower, worked_example
+from conftest import EPS, GOLDEN, lower, worked_example
 from paper_2411_09859_b200.inputs import skew_lower
 
 
@@ -240,3 +240,26 @@ def test_solve_singular_fixture(golden, n):
     g = golden("solve_small.npz")
     with pytest.raises(ZeroDivisionError, match=f"row {int(g[f'odd{n}_row'])}$"):
         oracle.solve(skew_lower(n, n), np.ones(n))
+
+
+@pytest.mark.parametrize("i", range(9))
+def test_skew_tridiag_gemm_fixture(golden, i):
+    """oracle.skew_tridiag_gemm (beta = 1 restatement) vs the reference's
+    kernels3.skew_tridiag_gemm outputs (l3_small.npz)."""
+    import sys
+    sys.path.insert(0, str(GOLDEN))
+    from l3_cases import L3_CASES, l3_inputs
+    g = golden("l3_small.npz")
+    p, q, k, tril, alpha, beta = L3_CASES[i]
+    a, b, tau, c = l3_inputs(i, p, q, k)
+    assert np.array_equal(g[f"c{i}_meta"][:3], [p, q, k])
+    want = g[f"c{i}_out"]
+    got = c.copy(order="F")
+    if beta != 1.0:   # the restatement has beta = 1; apply beta on the written part first
+        mask = np.tril(np.ones((p, q), bool), -1) if tril else np.ones((p, q), bool)
+        got[mask] *= beta
+    oracle.skew_tridiag_gemm(got, alpha, a, tau, b, tril=tril)
+    assert np.allclose(got, want, rtol=1e-13, atol=1e-13 * max(k, 1))
+    if tril:   # nothing on or above the diagonal moves
+        up = ~np.tril(np.ones((p, q), bool), -1)
+        assert np.array_equal(want[up], c[up])
