@@ -38,7 +38,7 @@ typedef enum {
 } skl_status;
 
 /* trailing-update scheme of the pivoted blocked driver (blocked.py:35) */
-enum { SKL_VAR1 = 0, SKL_VAR2A = 1, SKL_VAR2B = 2 };
+enum { SKL_VAR1 = 0, SKL_VAR2A = 1, SKL_VAR2B = 2, SKL_LEFT = 3 /* skl_ltlt_blk, unpivoted only */ };
 enum { SKL_F64 = 0, SKL_F32 = 1 };
 
 const char* skl_version(void);

@@ -16,7 +16,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "_lib" / "libskewltl_b200.so"
 
 SKL_OK, SKL_ZERO_PIVOT, SKL_BAD_ARGUMENT, SKL_ALIAS, SKL_CUDA_ERROR, SKL_UNSUPPORTED, SKL_BAD_PIVOT = range(7)
-SKL_VAR1, SKL_VAR2A, SKL_VAR2B = 0, 1, 2
+SKL_VAR1, SKL_VAR2A, SKL_VAR2B, SKL_LEFT = 0, 1, 2, 3
 SKL_F64, SKL_F32 = 0, 1
 VARIANT_CODES = {"var1": SKL_VAR1, "var2a": SKL_VAR2A, "var2b": SKL_VAR2B}
 

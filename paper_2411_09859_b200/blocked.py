@@ -174,7 +174,7 @@ def ltlt_blk_piv(x: SkewMatrixLower, b=DEFAULT_BLOCK, fused="var1", features=Non
 # driver and panel variant, replayed by instrument.flops_blk_unpivoted).
 # ---------------------------------------------------------------------------
 
-_GPU_SCHEDULE = {"var1": "var1", "var2a": "var2a", "var2b": "var2b", "twostep": "var2a", "left": "var2a"}
+_GPU_SCHEDULE = {"var1": "var1", "var2a": "var2a", "var2b": "var2b", "twostep": "var2a", "left": "left"}
 
 
 def _prep_input(x):
@@ -198,8 +198,10 @@ def _prep_input(x):
 def ltlt_blk_device(x, b=DEFAULT_BLOCK, fused="var1", pivot=False, out=None, stream=None):
     """Device entry of skl_ltlt_blk: returns ``(L, tau, piv, info)`` CUDA tensors
     without synchronising (``piv`` is None when unpivoted; ``info`` int32[1]:
-    first zero-pivot column + 1, 0 = success)."""
-    if fused not in PIVOTED_FUSED:
+    first zero-pivot column + 1, 0 = success).  ``fused="left"`` (unpivoted only)
+    runs the blocked left-looking driver: skew_tridiag_gemm(tril) into each
+    panel, no trailing update (blocked.py:236-265)."""
+    if fused not in PIVOTED_FUSED and not (fused == "left" and not pivot):
         raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
     _check_block(b)
     t = dv.require_cuda()
@@ -212,7 +214,7 @@ def ltlt_blk_device(x, b=DEFAULT_BLOCK, fused="var1", pivot=False, out=None, str
     piv = t.empty(m, dtype=t.int64, device=x.device) if pivot else None
     info = t.zeros(1, dtype=t.int32, device=x.device)
     lib = _capi.load()
-    code = _capi.VARIANT_CODES[fused]
+    code = _capi.SKL_LEFT if fused == "left" else _capi.VARIANT_CODES[fused]
     nbytes = lib.skl_ltlt_blk_piv_workspace_size(m, int(b), code)
     if nbytes == 0:
         raise InvalidVariant("configuration not supported by the GPU panel kernel")
@@ -269,10 +271,11 @@ def ltlt_blk_twostep(x: SkewMatrixLower, b=DEFAULT_BLOCK, panel_variant="ll", fe
 
 def ltlt_blk_left(x: SkewMatrixLower, b=DEFAULT_BLOCK, pivot=False, panel_variant="ll",
                   features=None) -> FactorizationResult:
-    """Blocked left-looking factorization (blocked.py:236-265).  Pivoting is
-    impossible at the blocked level (PivotUnsupported, blocked.py:247-248); the
-    unpivoted factors are computed by the right-looking GPU driver (the same
-    factorization; the tally is the left-looking one)."""
+    """Blocked left-looking factorization (blocked.py:236-265): before each panel
+    the GPU pulls every prior coupling into the panel's columns with the
+    skew_tridiag_gemm(tril) kernel (kernels3.py:239-302) and never touches the
+    trailing matrix.  Pivoting is impossible at the blocked level
+    (PivotUnsupported, blocked.py:247-248)."""
     if pivot:
         raise PivotUnsupported("a blocked pivoted left-looking algorithm cannot exist")
     return _blk_unpivoted(x, b, "left", panel_variant, features, "blk-left")

@@ -231,9 +231,14 @@ struct BlkWorkspace {
   double* pbuf;
   size_t ll_bytes;
   int k4cap, slot_words, np;
+  double* PL;  // left-looking driver: packed A = W[r:, 0:r] and (T B)^T of the panel rows
+  double* QL;
+  int* ltab;   // [np][owner_table_ints(kmax)] tile tables of the panel blocks
+  size_t ltab_stride;
 };
 
-size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base, BlkWorkspace* ws) {
+size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base, BlkWorkspace* ws,
+                  bool left = false) {
   Bump b(base);
   int kmax = 1, nelim_max = 1, ctas = 1;
   for (auto& p : plan) {
@@ -267,6 +272,19 @@ size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base,
   w.k4cap = k4cap;
   w.slot_words = slot_words;
   w.np = np;
+  if (left) {
+    size_t pl = 1, ql = 1;
+    for (auto& p : plan) {
+      const int k4 = (p.r + 3) / 4;
+      if (p.r < 2) continue;
+      pl = std::max(pl, skl::packed_elems(n - p.r, k4));
+      ql = std::max(ql, skl::packed_elems(p.nelim, k4));
+    }
+    w.PL = b.take<double>(pl);
+    w.QL = b.take<double>(ql);
+    w.ltab_stride = skl::owner_table_ints(kmax);
+    w.ltab = b.take<int>((size_t)std::max(np, 1) * w.ltab_stride);
+  }
   if (ws) *ws = w;
   return b.off + 256;
 }
@@ -408,7 +426,7 @@ int skl_skew_tridiag_gemm(int p, int q, int k, double alpha, const double* A, lo
   if (ntiles == 0) return SKL_OK;  // tril with q >= p... nothing strictly below the diagonal
   SKL_TRY(cudaMemcpyAsync(tab_dev, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, st));
   g_kt.launches += 2;
-  SKL_TRY(skl::launch_pack_gemm(A, lda, p, B, ldb, q, k, tau, alpha, k4cap, P, Q, st));
+  SKL_TRY(skl::launch_pack_gemm(A, lda, p, B, ldb, q, k, tau, alpha, k4cap, P, Q, st, 0));
   skl::ColOwner own{tab_dev, ntiles, 0, 1 << 30, 1, 0};
   SKL_TRY(skl::launch_gemm_lower(P, Q, k4cap, k4cap, nullptr, C, ldc, p, beta, st, &own, q, tril ? 1 : 0));
   return SKL_OK;
@@ -508,10 +526,11 @@ int skl_unpack_factor(int n, const double* X, long long ldx, double* L, long lon
 
 // ---------------------------------------------------------------------------
 size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant) {
-  if (n < 1 || nb < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B) return 0;
+  if (n < 1 || nb < 1 || variant < SKL_VAR1 || variant > SKL_LEFT) return 0;
+  const bool left = variant == SKL_LEFT;
   std::vector<PanelPlan> plan;
-  if (!make_schedule(n, nb, variant, plan)) return 0;
-  return layout_blk(n, nb, plan, nullptr, nullptr);
+  if (!make_schedule(n, nb, left ? SKL_VAR2A : variant, plan)) return 0;
+  return layout_blk(n, nb, plan, nullptr, nullptr, left);
 }
 
 namespace {
@@ -522,7 +541,13 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
                long long ldl, double* tau, long long* piv, int* info, void* workspace, size_t workspace_bytes,
                void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (variant < SKL_VAR1 || variant > SKL_VAR2B) return SKL_UNSUPPORTED;
+  if (variant < SKL_VAR1 || variant > SKL_LEFT) return SKL_UNSUPPORTED;
+  // blocked left-looking (blocked.py:236-265): every panel first pulls all prior
+  // couplings into its own columns (skew_tridiag_gemm, tril) and the trailing
+  // matrix is never updated; pivoting is impossible there (PivotUnsupported)
+  const bool left = variant == SKL_LEFT;
+  if (left && pivot) return SKL_UNSUPPORTED;
+  if (left) variant = SKL_VAR2A;  // the carry-column panel schedule
   if (n < 1 || nb < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
   if ((pivot && piv == nullptr) || (!pivot && info == nullptr)) return SKL_BAD_ARGUMENT;
   std::vector<PanelPlan> plan;
@@ -536,11 +561,20 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
         g_last_error = "the unpivoted drivers need the cluster panel kernels";
         return SKL_UNSUPPORTED;
       }
-  size_t need = layout_blk(n, nb, plan, nullptr, nullptr);
+  size_t need = layout_blk(n, nb, plan, nullptr, nullptr, left);
   if (workspace_bytes < need) return SKL_BAD_ARGUMENT;
   BlkWorkspace ws;
-  layout_blk(n, nb, plan, workspace, &ws);
+  layout_blk(n, nb, plan, workspace, &ws, left);
   const long long ld = n;
+  std::vector<int> ltiles;
+  if (left) {
+    std::vector<int> tabs((size_t)std::max((int)plan.size(), 1) * ws.ltab_stride, 0);
+    ltiles.assign(plan.size(), 0);
+    for (int k = 0; k < (int)plan.size(); ++k)
+      if (plan[k].r >= 2)
+        ltiles[k] = skl::build_rect_table(n - plan[k].r, plan[k].nelim, 1, tabs.data() + (size_t)k * ws.ltab_stride);
+    SKL_TRY(cudaMemcpyAsync(ws.ltab, tabs.data(), sizeof(int) * tabs.size(), cudaMemcpyHostToDevice, st));
+  }
 
   if (piv != nullptr) SKL_TRY(cudaMemsetAsync(piv, 0, sizeof(long long) * n, st));
   if (info != nullptr) SKL_TRY(cudaMemsetAsync(info, 0, sizeof(int), st));
@@ -564,6 +598,21 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
     const PanelPlan& p = plan[k];
     const int rt = p.r + p.nelim;
     const bool straggler = (variant == SKL_VAR1) && (n - rt >= 2);
+    if (left && p.r >= 2 && ltiles[k] > 0) {
+      // work[r:, r:r+be] -= work[r:, 0:r] T(tau[1:r]) work[r:r+be, 0:r]^T, row > col only
+      const int rr = p.r, k4 = (rr + 3) / 4;
+      {
+        KScope ks(KPACK, st);
+        SKL_TRY(skl::launch_pack_gemm(ws.W + rr, ld, n - rr, ws.W + rr, ld, p.nelim, rr, tau + 1, -1.0, k4, ws.PL,
+                                      ws.QL, st, 1));
+      }
+      {
+        KScope ks(KGEMM, st);
+        skl::ColOwner own{ws.ltab + (size_t)k * ws.ltab_stride, ltiles[k], 0, 1 << 30, 1, 0};
+        SKL_TRY(skl::launch_gemm_lower(ws.PL, ws.QL, k4, k4, nullptr, ws.W + (size_t)rr * ld + rr, ld, n - rr, 1.0,
+                                       st, &own, p.nelim, 1));
+      }
+    }
     skl::PanelArgs a{};
     a.W = ws.W;
     a.ld = ld;
@@ -608,7 +657,7 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
     tag += (uint32_t)p.nelim + 1;
 
     const int ntr = n - rt;
-    if (ntr >= 2) {
+    if (ntr >= 2 && !left) {
       const int ka = rt - p.lo;
       const int K = ka + (straggler ? 2 : 0);
       const int nk4 = (K + 3) / 4;

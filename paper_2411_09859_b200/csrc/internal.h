@@ -43,8 +43,10 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
 
 // skew_tridiag_gemm operands: P = alpha*A (p x k), Q = (T B)^T (q x k) with
 // B (k x q, column stride ldb) and T tridiag(t): Q[j,c] = t[c-1] B[c-1,j] - t[c] B[c+1,j]
+// btrans = 1: B is passed as B^T (q x k column-major, stride ldb)
 cudaError_t launch_pack_gemm(const double* A, long long lda, int p, const double* B, long long ldb, int q, int k,
-                             const double* t, double alpha, int k4cap, double* P, double* Q, cudaStream_t stream);
+                             const double* t, double alpha, int k4cap, double* P, double* Q, cudaStream_t stream,
+                             int btrans = 0);
 // C (p x q) *= beta on every entry (tri = 0) or on row > col only
 cudaError_t launch_scale_block(double* C, long long ldc, int p, int q, double beta, int tri, cudaStream_t stream);
 

@@ -396,7 +396,9 @@ __global__ void pack_rankk_kernel(const double* __restrict__ A, long long lda, i
 // (q rows) with Q[j, c] = t[c-1] B[c-1, j] - t[c] B[c+1, j]
 __global__ void pack_gemm_kernel(const double* __restrict__ A, long long lda, int p, const double* __restrict__ B,
                                  long long ldb, int q, int k, const double* __restrict__ t, double alpha, int k4cap,
-                                 double* __restrict__ P, double* __restrict__ Q) {
+                                 double* __restrict__ P, double* __restrict__ Q, int btrans) {
+  // btrans: B is given as B^T (q x k, column stride ldb), i.e. B[c, j] = B_arg[j + c*ldb]
+  const long long bs_row = btrans ? 1 : ldb, bs_col = btrans ? ldb : 1;
   const size_t totp = (size_t)tiles_for(p) * kTile * 4 * k4cap, totq = (size_t)tiles_for(q) * kTile * 4 * k4cap;
   const size_t total = totp > totq ? totp : totq;
   for (size_t off = blockIdx.x * (size_t)blockDim.x + threadIdx.x; off < total;
@@ -407,9 +409,9 @@ __global__ void pack_gemm_kernel(const double* __restrict__ A, long long lda, in
     if (off < totq) {
       double v = 0.0;
       if (row < q && col < k) {
-        const double* bj = B + (long long)row * ldb;
-        if (col >= 1) v = t[col - 1] * bj[col - 1];
-        if (col + 1 < k) v -= t[col] * bj[col + 1];
+        const double* bj = B + (long long)row * bs_row;
+        if (col >= 1) v = t[col - 1] * bj[(long long)(col - 1) * bs_col];
+        if (col + 1 < k) v -= t[col] * bj[(long long)(col + 1) * bs_col];
       }
       Q[off] = v;
     }
@@ -654,9 +656,11 @@ cudaError_t launch_pack_rankk(const double* A, long long lda, int rows, int ka, 
 }
 
 cudaError_t launch_pack_gemm(const double* A, long long lda, int p, const double* B, long long ldb, int q, int k,
-                             const double* t, double alpha, int k4cap, double* P, double* Q, cudaStream_t stream) {
+                             const double* t, double alpha, int k4cap, double* P, double* Q, cudaStream_t stream,
+                             int btrans) {
   const size_t total = std::max(packed_elems(p, k4cap), packed_elems(q, k4cap));
-  pack_gemm_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, p, B, ldb, q, k, t, alpha, k4cap, P, Q);
+  pack_gemm_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, p, B, ldb, q, k, t, alpha, k4cap, P, Q,
+                                                             btrans);
   return cudaGetLastError();
 }
 

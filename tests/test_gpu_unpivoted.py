@@ -132,3 +132,13 @@ def test_left_pivot_unsupported_and_bad_variants():
         pk().ltlt_unb_panel(X, 3, variant="rl", pivot=True)
     with pytest.raises(ValueError):
         pk().ltlt_blk_var1(X, b=0)
+
+
+@pytest.mark.parametrize("n,b", [(600, 128), (700, 96), (1000, 200)])
+def test_blocked_left_looking_larger(n, b):
+    """ltlt_blk_left on the GPU is the left-looking algorithm itself: per panel one
+    skew_tridiag_gemm(tril) of all prior couplings (several 128-row tiles, K = r
+    up to n) then the carry-column panel; no trailing update."""
+    x = skew_lower(n, 17 * n + b)
+    r = pk().ltlt_blk_left(pk().SkewMatrixLower(x), b=b)
+    assert_close(r, oracle.ltlt_blk(x, b, "left", "ll"), n, False)
