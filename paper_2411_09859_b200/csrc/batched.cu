@@ -103,9 +103,10 @@ __device__ void swap_and_eliminate(const BCtx<T>& c, int g, int b, T tau) {
     }
   }
   if (!sw) return;
-  // rows a, b of the older columns j < g
-  for (int j = tid; j < g; j += kBThreads) {
-    T* p = c.col(j);
+  // rows a, b of the older columns: only column g-1 now (the pair's fold reads
+  // it); columns j < g-1 get this interchange at write-back (deferred, composed)
+  if (tid == 0 && g >= 1) {
+    T* p = c.col(g - 1);
     T t = p[a];
     p[a] = p[b];
     p[b] = t;
@@ -117,36 +118,6 @@ __device__ void swap_and_eliminate(const BCtx<T>& c, int g, int b, T tau) {
     pa[i] = pb[i];
     pb[i] = t;
   }
-  for (int i = a + 1 + tid; i < b; i += kBThreads) {
-    T* pi = c.col(i);
-    T t = pi[b];
-    T u = pa[i];
-    pa[i] = -t;
-    pi[b] = -u;
-  }
-  if (tid == 0) pa[b] = -pa[b];
-}
-
-// X := P X P^T for the transposition (a, b), a < b, over the whole matrix
-template <typename T>
-__device__ void bsym_swap(const BCtx<T>& c, int a, int b) {
-  const int tid = threadIdx.x, n = c.n;
-  // rows a, b of columns j < a
-  for (int j = tid; j < a; j += kBThreads) {
-    T* p = c.col(j);
-    T t = p[a];
-    p[a] = p[b];
-    p[b] = t;
-  }
-  T* pa = c.col(a);
-  T* pb = c.col(b);
-  // columns a, b below row b
-  for (int i = b + 1 + tid; i < n; i += kBThreads) {
-    T t = pa[i];
-    pa[i] = pb[i];
-    pb[i] = t;
-  }
-  // crossing (i, a) <-> -(b, i), a < i < b
   for (int i = a + 1 + tid; i < b; i += kBThreads) {
     T* pi = c.col(i);
     T t = pi[b];
@@ -188,7 +159,9 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
   int* redi = reinterpret_cast<int*>(redv + 2 * kBWarps);
   T* vec = reinterpret_cast<T*>(smem_raw + kRedBytes);  // [2][n] rank-2 vectors
   int* cofs = reinterpret_cast<int*>(vec + 2 * n);      // [n] column offsets
-  T* store = reinterpret_cast<T*>(smem_raw + ((kRedBytes + 2 * n * sizeof(T) + n * sizeof(int) + 15) & ~size_t(15)));
+  int* qmap = cofs + n;                                  // [n] write-back position map
+  int* pvs = qmap + n;                                   // [n] relative pivots of this matrix
+  T* store = reinterpret_cast<T*>(smem_raw + ((kRedBytes + 2 * n * sizeof(T) + 3 * n * sizeof(int) + 15) & ~size_t(15)));
   const int tid = threadIdx.x;
   for (int j = tid; j < n; j += kBThreads) {
     // offset of column j >= J0: sum_{c=J0}^{j-1} (n-1-c), minus (j+1) so col(j)[i] indexes row i
@@ -217,7 +190,10 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
           l[(long long)j * ldl + i] = v;
       }
     }
-    if (tid == 0) pm[0] = 0;
+    if (tid == 0) {
+      pm[0] = 0;
+      pvs[0] = 0;
+    }
     __syncthreads();
 
     int nswaps = 0;
@@ -238,6 +214,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
       swap_and_eliminate(c, g, b, t0);
       if (tid == 0) {
         pm[g + 1] = b - (g + 1);
+        pvs[g + 1] = b - (g + 1);
         nswaps += b != g + 1;
         tm[g] = t0;
         if ((g & 1) == 0) {  // Pf = sign(P) prod_{i even} (-tau_i)
@@ -261,6 +238,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
       swap_and_eliminate(c, g + 1, b, t1);
       if (tid == 0) {
         pm[g + 2] = b - (g + 2);
+        pvs[g + 2] = b - (g + 2);
         nswaps += b != g + 2;
         tm[g + 1] = t1;
       }
@@ -332,22 +310,33 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         if (pf_logabs) pf_logabs[m] = sgn == 0.0 ? -INFINITY : logabs;
       }
     }
-    // write the packed columns back into L (flattened, coalesced)
-    {
-      const int nn = n * n;
-#pragma unroll 4
-      for (int e = tid; e < nn; e += kBThreads) {
-        const int j = e / n, i = e - j * n;
-        if (i > j && j >= J0) l[(long long)j * ldl + i] = c.col(j)[i];
-      }
-    }
+    // write-back.  Column j still lacks the row interchanges of steps >= j+2
+    // (swap_and_eliminate applies only step j+1's to it); walking j downwards,
+    // qmap = s_{n-2} o ... o s_{j+2} maps a stored position to its final row
+    // (the deferred row gather of apply_row_pivots, kernels2.py:232-271).
+    // Row j+1 (the explicit 1) and rows <= j are fixed by every later swap.
+    for (int i = tid; i < n; i += kBThreads) qmap[i] = i;
     __syncthreads();
+    for (int j = n - 2; j >= 0; --j) {
+      if (tid == 0 && j + 2 <= n - 2) {
+        const int a = j + 3, bb = j + 3 + pvs[j + 3];  // s_{j+2} swaps positions j+3 and its pivot row
+        const int t = qmap[a];
+        qmap[a] = qmap[bb];
+        qmap[bb] = t;
+      }
+      const T* cj = c.col(j);
+      // read the whole column, then scatter (columns j < J0 live in l itself)
+      for (int i = j + 1 + tid; i < n; i += kBThreads) vec[i] = cj[i];
+      __syncthreads();
+      for (int i = j + 1 + tid; i < n; i += kBThreads) l[(long long)j * ldl + qmap[i]] = vec[i];
+      __syncthreads();
+    }
   }
 }
 
 template <typename T>
 size_t batched_smem(int n, int J0) {
-  size_t head = (kRedBytes + 2 * n * sizeof(T) + n * sizeof(int) + 15) & ~size_t(15);
+  size_t head = (kRedBytes + 2 * n * sizeof(T) + 3 * n * sizeof(int) + 15) & ~size_t(15);
   long long cols = 0;
   for (int j = J0; j < n - 1; ++j) cols += n - 1 - j;
   return head + (size_t)cols * sizeof(T);
