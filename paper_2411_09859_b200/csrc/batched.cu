@@ -8,8 +8,14 @@
 // arithmetic -- inside ONE CTA: the trailing matrix lives in shared memory
 // (packed lower columns), the argmax is a warp redux over the column, the
 // symmetric interchange and the rank-2 update are CTA-parallel with only
-// __syncthreads between phases.  Columns that do not fit the shared-memory
-// budget (the first few columns in fp64) live in the output L buffer.
+// __syncthreads between phases.  The rank-2 updates are blocked: kKB pairs stay
+// pending (their w, l vectors in shared memory, interchanged with the matrix)
+// and reach the trailing matrix as one rank-2kKB pass, while the columns
+// eliminated in between get them applied on the fly (blocked.py:268-290's
+// W = A S + skew rank-2k, per CTA).  The older L columns take their row
+// interchanges once, at write-back (apply_row_pivots deferred and composed).
+// Columns that do not fit the shared-memory budget (the first columns) live
+// in the output L buffer.
 // A persistent grid walks the batch; outputs: L ("ones" layout), tau,
 // relative pivots, and sign / log|Pf| (overflow-free apps.py:26-30).
 #include <cmath>
@@ -23,10 +29,27 @@ namespace {
 #ifndef SKL_BATCHED_THREADS
 #define SKL_BATCHED_THREADS 256
 #endif
+// matrices (CTAs) per SM: measured 8192 x n=256 with 8 pending pairs -- fp64
+// 28.9 / 24.9 / 26.8 ms and fp32 21.8 / 18.6 / 16.9 ms for 2 / 3 / 4 per SM
 #ifndef SKL_BATCHED_PER_SM
-#define SKL_BATCHED_PER_SM 3
+#define SKL_BATCHED_PER_SM_F64 3
+#define SKL_BATCHED_PER_SM_F32 4
+#else
+#define SKL_BATCHED_PER_SM_F64 SKL_BATCHED_PER_SM
+#define SKL_BATCHED_PER_SM_F32 SKL_BATCHED_PER_SM
+#endif
+template <typename T>
+constexpr int per_sm() {
+  return sizeof(T) == 8 ? SKL_BATCHED_PER_SM_F64 : SKL_BATCHED_PER_SM_F32;
+}
+#ifndef SKL_BATCHED_KB
+#define SKL_BATCHED_KB 8  // fp64 31.5 / 26.4 / 24.9 / 35.5 ms (spills) for 2 / 4 / 8 / 16
 #endif
 constexpr int kBThreads = SKL_BATCHED_THREADS;
+// pending two-step pairs: the trailing matrix receives one rank-2*kKB update
+// every kKB pairs; the columns eliminated meanwhile get the pending pairs applied
+// on the fly (the blocked two-step of blocked.py:268-290 inside one CTA)
+constexpr int kKB = SKL_BATCHED_KB;
 constexpr int kBWarps = kBThreads / 32;
 constexpr size_t kRedBytes = 2 * kBWarps * (sizeof(double) + sizeof(int));
 
@@ -58,13 +81,24 @@ __device__ __forceinline__ int bwarp_argmax(double av, int idx, bool valid) {
 // iamax over X[g+1:, g] (ties -> lowest index).  One barrier: per-warp
 // partials in smem, then every warp reduces the partials redundantly.
 // `red` holds [2][kBWarps] (double-buffered by column parity).
+// pending pairs p < np: column j of the trailing matrix still lacks
+// sum_p (pw_p[i] pl_p[j] - pl_p[i] pw_p[j]) (pw/pl hold [kKB][n])
 template <typename T>
-__device__ int col_argmax(const BCtx<T>& c, int g, double* redv, int* redi) {
+__device__ __forceinline__ T pending_at(const T* pw, const T* pl, int n, int np, int i, int j) {
+  T acc = T(0);
+  for (int p = 0; p < np; ++p) acc += pw[p * n + i] * pl[p * n + j] - pl[p * n + i] * pw[p * n + j];
+  return acc;
+}
+
+template <typename T>
+__device__ int col_argmax(const BCtx<T>& c, int g, double* redv, int* redi, const T* pw = nullptr,
+                          const T* pl = nullptr, int np = 0) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const T* x = c.col(g);
+  T* x = c.col(g);
   double bv = -1.0;
   int bi = -1;
   for (int i = g + 1 + tid; i < c.n; i += kBThreads) {
+    if (np > 0) x[i] -= pending_at(pw, pl, c.n, np, i, g);  // column g becomes current
     double v = fabs((double)x[i]);
     if (v > bv) {
       bv = v;
@@ -89,10 +123,17 @@ __device__ int col_argmax(const BCtx<T>& c, int g, double* redv, int* redi) {
 // of column g: L[:, g] = X[:, g] / tau below the unit (tau = X[b, g] before the
 // interchange), explicit 1 at [a, g].  Element sets are disjoint, so one pass.
 template <typename T>
-__device__ void swap_and_eliminate(const BCtx<T>& c, int g, int b, T tau) {
+__device__ void swap_and_eliminate(const BCtx<T>& c, int g, int b, T tau, T* pw, T* pl, int np) {
   const int tid = threadIdx.x, n = c.n;
   const int a = g + 1;
   const bool sw = b != a;
+  // P (X - sum w l^T - l w^T) P^T: the pending vectors take the interchange too
+  if (sw && tid >= 32 && tid < 32 + 2 * np) {
+    T* v = (tid - 32 < np ? pw : pl) + ((tid - 32) % np) * n;
+    const T t = v[a];
+    v[a] = v[b];
+    v[b] = t;
+  }
   // column g: finalize
   T* xg = c.col(g);
   {
@@ -150,18 +191,21 @@ namespace {
 #endif
 
 template <typename T>
-__global__ void __launch_bounds__(kBThreads, SKL_BATCHED_PER_SM)
+__global__ void __launch_bounds__(kBThreads, per_sm<T>())
 batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx, long long strideX, T* __restrict__ L,
                long long ldl, long long strideL, T* __restrict__ tau, long long strideTau, long long* __restrict__ piv,
                long long stridePiv, double* __restrict__ pf_sign, double* __restrict__ pf_logabs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* redv = reinterpret_cast<double*>(smem_raw);  // [2][kBWarps] argmax partials
   int* redi = reinterpret_cast<int*>(redv + 2 * kBWarps);
-  T* vec = reinterpret_cast<T*>(smem_raw + kRedBytes);  // [2][n] rank-2 vectors
-  int* cofs = reinterpret_cast<int*>(vec + 2 * n);      // [n] column offsets
+  T* vec = reinterpret_cast<T*>(smem_raw + kRedBytes);  // [n] write-back staging
+  T* pw = vec + n;                                       // [kKB][n] pending w vectors
+  T* pl = pw + kKB * n;                                  // [kKB][n] pending l vectors
+  int* cofs = reinterpret_cast<int*>(pl + kKB * n);      // [n] column offsets
   int* qmap = cofs + n;                                  // [n] write-back position map
   int* pvs = qmap + n;                                   // [n] relative pivots of this matrix
-  T* store = reinterpret_cast<T*>(smem_raw + ((kRedBytes + 2 * n * sizeof(T) + 3 * n * sizeof(int) + 15) & ~size_t(15)));
+  T* store = reinterpret_cast<T*>(smem_raw + ((kRedBytes + (1 + 2 * kKB) * n * sizeof(T) + 3 * n * sizeof(int) + 15) &
+                                               ~size_t(15)));
   const int tid = threadIdx.x;
   for (int j = tid; j < n; j += kBThreads) {
     // offset of column j >= J0: sum_{c=J0}^{j-1} (n-1-c), minus (j+1) so col(j)[i] indexes row i
@@ -204,14 +248,16 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
     long long bpt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long bprev = clock64();
 #endif
+    int np = 0;  // pending two-step pairs (rows/cols >= their s0 = g_p + 3)
     while (g < end) {
       // ---- eliminate(g): argmax, interchange + scale in one pass -------------
+      // (column g is current: it was the previous pair's fold column)
       BMARK(7);
       int b = col_argmax(c, g, redv, redi);
       const T t0 = c.col(g)[b];  // becomes X[g+1, g] after the interchange
       __syncthreads();            // every warp has read the partials and tau
       BMARK(0);
-      swap_and_eliminate(c, g, b, t0);
+      swap_and_eliminate(c, g, b, t0, pw, pl, np);
       if (tid == 0) {
         pm[g + 1] = b - (g + 1);
         pvs[g + 1] = b - (g + 1);
@@ -230,12 +276,12 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
         g += 1;
         break;
       }
-      // ---- eliminate(g+1) -----------------------------------------------------
-      b = col_argmax(c, g + 1, redv, redi);
+      // ---- eliminate(g+1): the pending pairs are applied to column g+1 first --
+      b = col_argmax(c, g + 1, redv, redi, pw, pl, np);
       const T t1 = c.col(g + 1)[b];
       __syncthreads();
       BMARK(2);
-      swap_and_eliminate(c, g + 1, b, t1);
+      swap_and_eliminate(c, g + 1, b, t1, pw, pl, np);
       if (tid == 0) {
         pm[g + 2] = b - (g + 2);
         pvs[g + 2] = b - (g + 2);
@@ -244,7 +290,8 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
       }
       __syncthreads();
       BMARK(3);
-      // ---- fold the first coupling into column g+2, rank-2 vectors ----------
+      // ---- column g+2: pending pairs, then fold the first coupling; this pair's
+      // rank-2 vectors become pending entry np -----------------------------------
       const int s0 = g + 3;
       T* xg = c.col(g);
       T* x1 = c.col(g + 1);
@@ -253,44 +300,50 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
       for (int i = s0 + tid; i < n; i += kBThreads) {
         const T l2 = x1[i];
         const T l1i = xg[i];
-        const T f = x2[i] - t1 * (x20 * l2 - l1i);
+        const T x2i = np > 0 ? x2[i] - pending_at(pw, pl, n, np, i, g + 2) : x2[i];
+        const T f = x2i - t1 * (x20 * l2 - l1i);
         x2[i] = f;
-        vec[i] = f - t1 * l1i;  // wv
-        vec[n + i] = l2;
+        pw[np * n + i] = f - t1 * l1i;  // wv
+        pl[np * n + i] = l2;
       }
+      ++np;
       __syncthreads();
       BMARK(4);
       if (tid == 0) x1[g + 2] = T(1);
-      // ---- X[s:, s:] -= wv l2^T - l2 wv^T -------------------------------------
-      if (s0 < n) {
-        // flattened strictly-lower trapezoid of the trailing block, column-major
-        // lane <-> rows i = s0 + lane + 32 r (wv_i, l2_i held in registers),
-        // warp <-> columns j = s0 + warp + kBWarps q (l2_j, wv_j broadcast)
-        const int lane = tid & 31, warp = tid >> 5;
-        if (n - s0 <= 256) {
-          T vi[8], ui[8];
+      // ---- every kKB pairs: X[s:, s:] -= sum_p (w_p l_p^T - l_p w_p^T) ---------
+      if (np == kKB) {
+        // thread <-> row i (coalesced in every column; the pending row values in
+        // registers), columns j in [s0, i) walked in lockstep (broadcast reads of
+        // w_p[j], l_p[j]); loads of consecutive columns are independent
+        for (int i = s0 + 1 + tid; i < n; i += kBThreads) {  // empty once s0 >= n - 1
+          T wi[kKB], li[kKB];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const int i = s0 + lane + 32 * r;
-            vi[r] = i < n ? vec[i] : T(0);
-            ui[r] = i < n ? vec[n + i] : T(0);
+          for (int p = 0; p < kKB; ++p) {
+            wi[p] = pw[p * n + i];
+            li[p] = pl[p * n + i];
           }
-          for (int j = s0 + warp; j < n - 1; j += kBWarps) {
-            T* p = c.col(j);
-            const T wj = vec[j], lj = vec[n + j];
+          int j = s0;
+          for (; j + 1 < i; j += 2) {
+            T* c0 = c.col(j);
+            T* c1 = c.col(j + 1);
+            T v0 = c0[i], v1 = c1[i];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-              const int i = s0 + lane + 32 * r;
-              if (i > j && i < n) p[i] -= vi[r] * lj - ui[r] * wj;
+            for (int p = 0; p < kKB; ++p) {
+              v0 -= wi[p] * pl[p * n + j] - li[p] * pw[p * n + j];
+              v1 -= wi[p] * pl[p * n + j + 1] - li[p] * pw[p * n + j + 1];
             }
+            c0[i] = v0;
+            c1[i] = v1;
           }
-        } else {
-          for (int j = s0 + warp; j < n - 1; j += kBWarps) {
-            T* p = c.col(j);
-            const T wj = vec[j], lj = vec[n + j];
-            for (int i = j + 1 + lane; i < n; i += 32) p[i] -= vec[i] * lj - vec[n + i] * wj;
+          if (j < i) {
+            T* c0 = c.col(j);
+            T v0 = c0[i];
+#pragma unroll
+            for (int p = 0; p < kKB; ++p) v0 -= wi[p] * pl[p * n + j] - li[p] * pw[p * n + j];
+            c0[i] = v0;
           }
         }
+        np = 0;
       }
       __syncthreads();
       BMARK(5);
@@ -336,7 +389,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
 
 template <typename T>
 size_t batched_smem(int n, int J0) {
-  size_t head = (kRedBytes + 2 * n * sizeof(T) + 3 * n * sizeof(int) + 15) & ~size_t(15);
+  size_t head = (kRedBytes + (1 + 2 * kKB) * n * sizeof(T) + 3 * n * sizeof(int) + 15) & ~size_t(15);
   long long cols = 0;
   for (int j = J0; j < n - 1; ++j) cols += n - 1 - j;
   return head + (size_t)cols * sizeof(T);
@@ -352,14 +405,15 @@ cudaError_t launch_batched(int batch, int n, const T* X, long long ldx, long lon
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // SKL_BATCHED_PER_SM matrices share an SM (each CTA gets 1/k of the shared memory)
-  const size_t budget = SKL_BATCHED_PER_SM == 1 ? (size_t)lim : (size_t)(228 * 1024) / SKL_BATCHED_PER_SM - 1024;
+  // per_sm<T>() matrices share an SM (each CTA gets 1/k of the shared memory)
+  constexpr int kPerSm = per_sm<T>();
+  const size_t budget = kPerSm == 1 ? (size_t)lim : (size_t)(228 * 1024) / kPerSm - 1024;
   int J0 = 0;
   while (J0 < n - 1 && batched_smem<T>(n, J0) > budget) ++J0;
   size_t smem = batched_smem<T>(n, J0);
   cudaError_t e = cudaFuncSetAttribute(batched_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  long long g = (long long)nsm * SKL_BATCHED_PER_SM;
+  long long g = (long long)nsm * kPerSm;
   int grid = batch < g ? batch : (int)g;
   batched_kernel<T><<<grid, kBThreads, smem, stream>>>(batch, n, J0, X, ldx, strideX, L, ldl, strideL, tau, strideTau,
                                                        piv, stridePiv, pf_sign, pf_logabs);
