@@ -1071,6 +1071,13 @@ int skl_ltlt_batched_piv(int batch, int n, int dtype, const void* X, long long l
   if (batch < 0 || n < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (batch == 0) return SKL_OK;
+  {
+    // L is written while X is still read (the upper triangle is copied last)
+    const size_t es = dtype == SKL_F32 ? sizeof(float) : sizeof(double);
+    const size_t xb = es * (size_t)((long long)(batch - 1) * strideX + ldx * (n - 1) + n);
+    const size_t lb = es * (size_t)((long long)(batch - 1) * strideL + ldl * (n - 1) + n);
+    if (overlaps(X, xb, L, lb)) return SKL_ALIAS;
+  }
   if (dtype == SKL_F64) {
     SKL_TRY(skl::launch_batched<double>(batch, n, static_cast<const double*>(X), ldx, strideX,
                                         static_cast<double*>(L), ldl, strideL, static_cast<double*>(tau), n - 1,
