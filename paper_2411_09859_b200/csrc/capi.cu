@@ -1071,6 +1071,10 @@ int skl_ltlt_batched_piv(int batch, int n, int dtype, const void* X, long long l
   if (batch < 0 || n < 1 || ldx < n || ldl < n) return SKL_BAD_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (batch == 0) return SKL_OK;
+  if (n > 512) {
+    g_last_error = "batched factorization: n > 512 (one CTA per matrix, at most two rows per thread)";
+    return SKL_UNSUPPORTED;
+  }
   {
     // L is written while X is still read (the upper triangle is copied last)
     const size_t es = dtype == SKL_F32 ? sizeof(float) : sizeof(double);

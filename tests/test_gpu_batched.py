@@ -67,3 +67,55 @@ def test_config4_f32_golden(golden):
     assert np.mean(sign == g["sign"]) >= 0.99
     rel = np.abs(logabs - g["logpf"]) / np.abs(g["logpf"])
     assert np.median(rel) <= 1e-5 and np.max(rel) <= 1e-3
+
+
+@pytest.mark.parametrize("n", [257, 300, 512])
+def test_batched_two_rows_per_thread(n):
+    """n > 256: every thread owns two physical rows (RPT = 2 instantiation)."""
+    xs = np.stack([skew_lower(n, 300 + i) for i in range(3)])
+    L, tau, piv, sign, logabs = apps().ltlt_batched_piv(xs)
+    for i in range(3):
+        o = oracle.ltlt_blk_piv(xs[i], b=n)
+        assert np.array_equal(piv[i], o.pivots)
+        assert np.allclose(tau[i], o.tau, rtol=1e-10 * n, atol=1e-10 * n)
+        assert np.max(np.abs(np.tril(L[i], -1) - np.tril(o.work, -1))) <= 1e-10 * n
+        assert np.array_equal(np.triu(L[i]), np.triu(xs[i]))
+        s, lg = oracle.pfaffian_slog(o.tau, o.pivots, n)
+        assert sign[i] == s
+        if n % 2 == 0:
+            assert abs(logabs[i] - lg) <= 1e-10 * max(abs(lg), 1.0)
+
+
+def test_batched_zero_columns_and_rank_deficient():
+    """All-zero subcolumns (tau = 0, elimination continues) and a rank-deficient
+    matrix (Pf = 0) inside one batch, against the oracle."""
+    n = 40
+    a = skew_lower(n, 7)
+    a[:, 5] = 0.0
+    a[5, :] = 0.0          # row/column 5 zero: singular, a zero tau appears
+    b = np.zeros((n, n))   # everything zero
+    c = skew_lower(n, 8)
+    xs = np.stack([a, b, c])
+    L, tau, piv, sign, logabs = apps().ltlt_batched_piv(xs)
+    for i in range(3):
+        o = oracle.ltlt_blk_piv(xs[i], b=n)
+        assert np.array_equal(piv[i], o.pivots)
+        assert np.allclose(tau[i], o.tau, rtol=1e-10 * n, atol=1e-10 * n)
+        assert np.max(np.abs(np.tril(L[i], -1) - np.tril(o.work, -1))) <= 1e-10 * n
+    assert sign[0] == 0.0 and sign[1] == 0.0 and sign[2] != 0.0
+
+
+def test_batched_rejects_aliasing_and_large_n():
+    import torch
+    from paper_2411_09859_b200 import _capi
+    lib = _capi.load()
+    xd = torch.zeros((2, 8, 8), dtype=torch.float64, device="cuda")
+    tau = torch.empty((2, 8), dtype=torch.float64, device="cuda")
+    piv = torch.empty((2, 8), dtype=torch.int64, device="cuda")
+    st = lib.skl_ltlt_batched_piv(2, 8, _capi.SKL_F64, xd.data_ptr(), 8, 64, xd.data_ptr(), 8, 64, tau.data_ptr(),
+                                  piv.data_ptr(), None, None, None)
+    assert st == 3  # SKL_ALIAS
+    big = torch.zeros((1, 513, 513), dtype=torch.float64, device="cuda")
+    with pytest.raises(Exception):
+        apps().ltlt_batched_piv_device(big)
+        torch.cuda.synchronize()
