@@ -140,6 +140,21 @@ __device__ __forceinline__ void load_pend_row(float* q, const float* src) {
   }
 }
 
+// sum_k (w_k q_l,k - l_k q_w,k) with four independent FMA chains (the pass is
+// otherwise bound by the dependent-DFMA latency)
+template <typename T>
+__device__ __forceinline__ T pair_dot(const T* wp, const T* lp, const T* q) {
+  T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+#pragma unroll
+  for (int k = 0; k < kKB; k += 2) {
+    a0 = fma(wp[k], q[kKB + k], a0);
+    a1 = fma(lp[k], q[k], a1);
+    a2 = fma(wp[k + 1], q[kKB + k + 1], a2);
+    a3 = fma(lp[k + 1], q[k + 1], a3);
+  }
+  return (a0 + a2) - (a1 + a3);
+}
+
 template <typename T, int RPT>
 struct RowState {
   T cur[RPT];  // current column value of this physical row
@@ -425,8 +440,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
             for (int t2 = 0; t2 < U; ++t2) {
               T q[2 * kKB];
               load_pend_row(q, pend + (size_t)actl[c + t2] * PS);
-#pragma unroll
-              for (int k = 0; k < kKB; ++k) v[t2] -= wp[k] * q[kKB + k] - lp[k] * q[k];
+              v[t2] -= pair_dot(wp, lp, q);
               *e[t2] = v[t2];
             }
           }
@@ -435,8 +449,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
             T v0 = *e0;
             T q[2 * kKB];
             load_pend_row(q, pend + (size_t)actl[c] * PS);
-#pragma unroll
-            for (int k = 0; k < kKB; ++k) v0 -= wp[k] * q[kKB + k] - lp[k] * q[k];
+            v0 -= pair_dot(wp, lp, q);
             *e0 = v0;
           }
         }
