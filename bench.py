@@ -236,6 +236,41 @@ def config5_single(torch, pk, dv, fp64_peak, e0, e1):
             "input": "X=G-G^T, G~N(0,1/n) torch CUDA generator seed 0 (device-generated)"}
 
 
+def config4_sharded(torch, world, rank):
+    """Config 4 across the N ranks: rank r factors the contiguous slice of the 8192
+    matrices that parallel.shard_range gives it (global per-matrix seeds), no
+    communication during compute.  Device time, max over ranks; whole-job rate."""
+    from paper_2411_09859_b200 import apps
+    from paper_2411_09859_b200.inputs import skew_lower
+    from paper_2411_09859_b200.parallel import shard_range
+    B, n = 8192, 256
+    lo, hi = shard_range(B, rank, world)
+    xs = np.stack([skew_lower(n, i) for i in range(lo, hi)])
+    out = {}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for name, dt in (("f64", np.float64), ("f32", np.float32)):
+        xd = torch.from_numpy(np.ascontiguousarray(np.swapaxes(xs.astype(dt), 1, 2))).cuda()
+        for _ in range(2):
+            apps.ltlt_batched_piv_device(xd)
+        times = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            barrier(world)
+            e0.record()
+            apps.ltlt_batched_piv_device(xd)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = max_over_ranks(world, statistics.median(times))
+        out[name] = {"ms": round(ms, 3), "gflops": round(B * n ** 3 / 3 / (ms * 1e-3) / 1e9, 1),
+                     "pfaffians_per_s": round(B / (ms * 1e-3), 0)}
+        del xd
+    torch.cuda.empty_cache()
+    out.update({"ranks": world, "matrices_per_rank": hi - lo, "scaling": "strong (8192 matrices split)",
+                "communication": "none during compute"})
+    return out
+
+
 def config5_distributed(torch, world, rank, fp64_peak):
     """Config 5 over the N ranks: block-cyclic columns (nbd=512), VMM-mapped peer
     blocks, NCCL stream barrier (skl_ltlt_blk_piv_dist).  Device time, max over ranks."""
@@ -522,6 +557,10 @@ def main():
         timer = threading.Timer(600.0, watchdog)
         timer.daemon = True
         timer.start()
+        try:
+            line["other_configs"]["config4_sharded_8192x256"] = config4_sharded(torch, world, rank)
+        except Exception as exc:  # noqa: BLE001 -- reported in the line
+            line["other_configs"]["config4_sharded_8192x256"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         try:
             del flush
             torch.cuda.empty_cache()

@@ -5,9 +5,9 @@
   global indices), computes them on its own GPU with the batched kernel, and
   the per-matrix (sign, log|Pf|) are all-gathered -- no communication during
   compute.
-* A single matrix (configs 2/3) is run as independent replicas (no
-  collective); the 1-D block-cyclic multi-GPU factorization of config 5 is not
-  built this round.
+* A single matrix of configs 2/3 is run as independent replicas (no
+  collective); config 5's one large matrix uses the 1-D block-cyclic driver in
+  dist.py (peer-mapped column blocks, one stream barrier per panel phase).
 
 The compute function is injectable so the host logic can be tested on CPU
 with the gloo backend.
