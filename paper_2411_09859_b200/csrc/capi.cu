@@ -121,7 +121,10 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   static int gpu_nb = env_int("SKL_GPU_NB", 96);
   static int no_cluster = env_int("SKL_NO_CLUSTER", 0);
   const int Cmax = no_cluster ? 0 : skl::panel_cluster_size();
-  if (Cmax > 0) {
+  // SKL_FORCE_MULTI=1: skip the single-cluster plan (tests drive the multi-cluster
+  // exchange at small n with it; SKL_MULTI_Q caps the cluster count)
+  static int force_multi = env_int("SKL_FORCE_MULTI", 0);
+  if (Cmax > 0 && !force_multi) {
     // smallest cluster that keeps <= rows_target rows per CTA: fewer CTAs means a
     // cheaper cluster barrier and less DSMEM fan-out of the pivot row per step
     static int rows_target = env_int("SKL_CLUSTER_ROWS", 16);

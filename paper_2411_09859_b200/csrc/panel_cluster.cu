@@ -383,7 +383,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       const CCand mine = lane < C ? s.cand[par * kClusterMax + lane] : CCand{0.0, -1, -1};
       const int id = warp_argmax_redux(mine.v, mine.idx, ok);
       owner = __ffs(__ballot_sync(0xffffffffu, ok && mine.idx == id)) - 1;
-      w = s.cand[par * kClusterMax + owner];
+      if (owner < 0) {  // no row of this cluster is below g (small multi-cluster panels)
+        w = CCand{0.0, -1, -1};
+        owner = 0;
+      } else {
+        w = s.cand[par * kClusterMax + owner];
+      }
       owner += qid * C;  // global CTA id of the cluster's best
     }
     if (MULTI && Q > 1) {
