@@ -42,10 +42,12 @@ def pfaffian(x: SkewMatrixLower, b=None):
     if m % 2:
         return 0.0
     res = ltlt_blk_piv(x, b=b or min(DEFAULT_BLOCK, m))
-    tau = res.t.tau.detach().cpu().numpy() if hasattr(res.t.tau, "detach") else res.t.tau
-    val = float(res.p.sign())
+    tau = res.t.tau.detach().cpu().numpy() if hasattr(res.t.tau, "detach") else np.asarray(res.t.tau)
+    # the product runs in tau's dtype, like the reference's numpy scalars: a float32
+    # input overflows to inf exactly where the reference's does (pfaffian_slog does not)
+    val = res.p.sign()
     for i in range(0, m - 1, 2):
-        val = val * (-float(tau[i]))
+        val = val * (-tau[i])
     return val
 
 
@@ -57,14 +59,15 @@ def solve(x: SkewMatrixLower, b, block=None, tol_scale=10.0):
     columns.  Raises SingularT for a numerically singular X (every odd m)."""
     from . import _capi
     from . import device as dv
-    from .blocked import ltlt_blk_piv_device
+    from .blocked import _device_input, ltlt_blk_piv_device
     from .core import SingularT
 
     if not isinstance(x, SkewMatrixLower):
         x = SkewMatrixLower(x)
     m = x.m
     t = dv.require_cuda()
-    on_device = dv.is_colmajor_cuda(x.data)
+    if not dv.is_colmajor_cuda(x.data) and np.asarray(x.data).dtype not in (np.float64, np.float32):
+        x = SkewMatrixLower(np.asarray(x.data, dtype=np.float64))
     bd_in = b if dv._is_cuda_tensor(b) else None
     bh = None if bd_in is not None else np.asarray(b, dtype=float)
     one_d = (bd_in.dim() if bd_in is not None else bh.ndim) == 1
@@ -80,13 +83,7 @@ def solve(x: SkewMatrixLower, b, block=None, tol_scale=10.0):
             raise ValueError("dimension mismatch")
         bdev = dv.to_device_colmajor(rhs)
     nrhs = int(bdev.shape[1])
-    if on_device:
-        xd = x.data
-    else:
-        host = np.asarray(x.data)
-        if host.dtype != np.float64:
-            host = host.astype(np.float64)
-        xd = dv.to_device_colmajor(host)
+    xd, _, _ = _device_input(x, "solve")
     L, tau, piv = ltlt_blk_piv_device(xd, b=block or min(DEFAULT_BLOCK, m), fused="var1")
     if nrhs == 0:
         out = bdev

@@ -16,7 +16,7 @@ import numpy as np
 from . import _capi
 from . import device as dv
 from .core import (InvalidVariant, PermutationVector, PivotUnsupported, SkewMatrixLower, SkewTridiagonal,
-                   UnitLowerFactor, ZeroPivot)
+                   UnitLowerFactor, ZeroPivot, _is_torch)
 from .instrument import FlopCounter, flops_blk_piv, flops_blk_unpivoted
 
 DEFAULT_BLOCK = 256                               # blocked.py:34
@@ -43,6 +43,46 @@ class FactorizationResult:
     t: SkewTridiagonal
     p: PermutationVector
     flops: FlopCounter
+
+
+def _device_input(x, who="the GPU path"):
+    """SkewMatrixLower data -> (column-major float64 CUDA tensor, on_device, dt).
+
+    float32 input (the reference runs it end to end, SURVEY 8b "Dtypes") is
+    factored in float64 on the device and the factors are rounded back to float32
+    (``dt``; None for float64) by ``_narrow``: L and tau keep the input dtype like
+    the reference's, computed with fp64 arithmetic.  Pivots can then differ from
+    the reference's float32 run only at float32-rounding near-ties."""
+    if dv.is_colmajor_cuda(x.data):
+        t = dv.torch()
+        if x.data.dtype == t.float64:
+            return x.data, True, None
+        if x.data.dtype == t.float32:
+            xd = dv.empty_colmajor(x.m, x.m, t.float64)
+            xd.copy_(x.data)
+            return xd, True, t.float32
+        raise TypeError(f"{who} serves float64 and float32")
+    host = np.asarray(x.data)
+    if host.dtype == object:
+        raise TypeError("exact (object) dtypes are served by the reference, not the GPU path")
+    if host.dtype == np.float64:
+        return dv.to_device_colmajor(host), False, None
+    if host.dtype == np.float32:
+        return dv.to_device_colmajor(host.astype(np.float64)), False, np.float32
+    raise TypeError(f"{who} serves float64 and float32")
+
+
+def _narrow(res, dt):
+    """Round a FactorizationResult's L and tau to the input dtype (float32 input)."""
+    if dt is None:
+        return res
+    L, tau = res.l.data, res.t.tau
+    if _is_torch(L):
+        L, tau = L.to(dt), tau.to(dt)
+    else:
+        L, tau = np.asarray(L, dtype=dt, order="F"), np.asarray(tau, dtype=dt)
+    return FactorizationResult(UnitLowerFactor(L, res.l.mode, res.l.first_column), SkewTridiagonal(tau), res.p,
+                               res.flops)
 
 
 def _check_block(b):
@@ -141,27 +181,16 @@ def ltlt_blk_piv(x: SkewMatrixLower, b=DEFAULT_BLOCK, fused="var1", features=Non
     m = x.m
     if m < 1:
         raise ValueError("m >= 1 required")
-    on_device = dv.is_colmajor_cuda(x.data)
-    if on_device:
-        xd = x.data
-        if xd.dtype != dv.torch().float64:
-            raise TypeError("the blocked GPU path computes in float64")
-    else:
-        host = np.asarray(x.data)
-        if host.dtype == object:
-            raise TypeError("exact (object) dtypes are served by the reference, not the GPU path")
-        if host.dtype != np.float64:
-            raise TypeError("the blocked GPU path computes in float64")
-        xd = dv.to_device_colmajor(host)
+    xd, on_device, dt = _device_input(x, "the blocked GPU path")
     L, tau, piv = ltlt_blk_piv_device(xd, b, fused)
     piv_h = piv.cpu().numpy()
     tau_h = tau.cpu().numpy()
     flops = flops_blk_piv(m, b, fused, piv_h, tau_h)
     if on_device:
-        return FactorizationResult(UnitLowerFactor(L, "ones"), SkewTridiagonal(tau), PermutationVector(piv_h, m),
-                                   flops)
-    return FactorizationResult(UnitLowerFactor(dv.to_host_colmajor(L), "ones"), SkewTridiagonal(tau_h),
-                               PermutationVector(piv_h, m), flops)
+        return _narrow(FactorizationResult(UnitLowerFactor(L, "ones"), SkewTridiagonal(tau),
+                                           PermutationVector(piv_h, m), flops), dt)
+    return _narrow(FactorizationResult(UnitLowerFactor(dv.to_host_colmajor(L), "ones"), SkewTridiagonal(tau_h),
+                                       PermutationVector(piv_h, m), flops), dt)
 
 
 # ---------------------------------------------------------------------------
@@ -183,16 +212,8 @@ def _prep_input(x):
     m = x.m
     if m < 1:
         raise ValueError("m >= 1 required")
-    if dv.is_colmajor_cuda(x.data):
-        if x.data.dtype != dv.torch().float64:
-            raise TypeError("the blocked GPU path computes in float64")
-        return x, x.data, True
-    host = np.asarray(x.data)
-    if host.dtype == object:
-        raise TypeError("exact (object) dtypes are served by the reference, not the GPU path")
-    if host.dtype != np.float64:
-        raise TypeError("the blocked GPU path computes in float64")
-    return x, dv.to_device_colmajor(host), False
+    xd, on_device, dt = _device_input(x, "the blocked GPU path")
+    return x, xd, on_device, dt
 
 
 def ltlt_blk_device(x, b=DEFAULT_BLOCK, fused="var1", pivot=False, out=None, stream=None):
@@ -233,7 +254,7 @@ def _blk_unpivoted(x, b, driver, panel_variant, features, who):
     f = features or Features()
     if driver != "var1" and not f.external_t:
         raise InvalidVariant(f"{who} needs tau in an external vector (external_t)")
-    x, xd, on_device = _prep_input(x)
+    x, xd, on_device, dt = _prep_input(x)
     m = x.m
     L, tau, _piv, info = ltlt_blk_device(xd, b, _GPU_SCHEDULE[driver], pivot=False)
     code = int(info.item())
@@ -243,8 +264,8 @@ def _blk_unpivoted(x, b, driver, panel_variant, features, who):
     l_host = None if on_device and driver != "twostep" else dv.to_host_colmajor(L)
     flops = flops_blk_unpivoted(m, b, driver, panel_variant, tau_h, l_host)
     l_out = L if on_device else l_host
-    return FactorizationResult(UnitLowerFactor(l_out, "ones"), SkewTridiagonal(tau if on_device else tau_h),
-                               PermutationVector(np.zeros(0, dtype=np.int64), m), flops)
+    return _narrow(FactorizationResult(UnitLowerFactor(l_out, "ones"), SkewTridiagonal(tau if on_device else tau_h),
+                                       PermutationVector(np.zeros(0, dtype=np.int64), m), flops), dt)
 
 
 def ltlt_blk_var1(x: SkewMatrixLower, b=DEFAULT_BLOCK, panel_variant="ll", features=None) -> FactorizationResult:

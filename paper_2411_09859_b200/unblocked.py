@@ -20,27 +20,22 @@ import numpy as np
 
 from . import _capi
 from . import device as dv
-from .blocked import PANEL_VARIANTS, FactorizationResult, ltlt_blk_device, ltlt_blk_piv_device
+from .blocked import (PANEL_VARIANTS, FactorizationResult, _device_input, _narrow, ltlt_blk_device,
+                      ltlt_blk_piv_device)
 from .core import (InvalidVariant, PermutationVector, SkewMatrixLower, SkewTridiagonal, UnitLowerFactor,
                    ZeroPivot, _is_torch)
 from .instrument import flops_unb_ll, flops_unb_panel, flops_unb_rl, flops_unb_twostep
 
 
 def _prep(x):
+    """-> (x, float64 column-major CUDA input, on_device, dt); float32 input is
+    factored in float64 and rounded back (blocked._device_input / _narrow)."""
     if not isinstance(x, SkewMatrixLower):
         x = SkewMatrixLower(x)
     if x.m < 1:
         raise ValueError("m >= 1 required")
-    if dv.is_colmajor_cuda(x.data):
-        if x.data.dtype != dv.torch().float64:
-            raise TypeError("the GPU path computes in float64")
-        return x, x.data, True
-    host = np.asarray(x.data)
-    if host.dtype == object:
-        raise TypeError("exact (object) dtypes are served by the reference, not the GPU path")
-    if host.dtype != np.float64:
-        raise TypeError("the GPU path computes in float64")
-    return x, dv.to_device_colmajor(host), False
+    xd, on_device, dt = _device_input(x)
+    return x, xd, on_device, dt
 
 
 def ltlt_unb_twostep_device(xd, pivot=False, out=None, stream=None):
@@ -66,7 +61,7 @@ def ltlt_unb_twostep_device(xd, pivot=False, out=None, stream=None):
 
 def ltlt_unb_twostep(x: SkewMatrixLower, pivot=False) -> FactorizationResult:
     """Two-step right-looking factorization (unblocked.py:229-240)."""
-    x, xd, on_device = _prep(x)
+    x, xd, on_device, dt = _prep(x)
     m = x.m
     L, tau, piv, info = ltlt_unb_twostep_device(xd, pivot)
     code = int(info.item())
@@ -77,8 +72,8 @@ def ltlt_unb_twostep(x: SkewMatrixLower, pivot=False) -> FactorizationResult:
     flops = flops_unb_twostep(m, piv.cpu().numpy(), tau_h, pivot=pivot)
     l_out = L if on_device else dv.to_host_colmajor(L)
     t_out = tau if on_device else tau_h
-    return FactorizationResult(UnitLowerFactor(l_out, "ones"), SkewTridiagonal(t_out), PermutationVector(piv_h, m),
-                               flops)
+    return _narrow(FactorizationResult(UnitLowerFactor(l_out, "ones"), SkewTridiagonal(t_out),
+                                       PermutationVector(piv_h, m), flops), dt)
 
 
 def _apply_first_column_device(xd, first_column):
@@ -112,11 +107,11 @@ def _unpivoted_full(xd, m):
     return L, tau
 
 
-def _result(L, tau_h, tau, piv_h, m, fc, on_device, first_column=None):
+def _result(L, tau_h, tau, piv_h, m, fc, on_device, first_column=None, dt=None):
     l_out = L if on_device else dv.to_host_colmajor(L)
     t_out = tau if on_device else tau_h
-    return FactorizationResult(UnitLowerFactor(l_out, "ones", first_column), SkewTridiagonal(t_out),
-                               PermutationVector(piv_h, m), fc)
+    return _narrow(FactorizationResult(UnitLowerFactor(l_out, "ones", first_column), SkewTridiagonal(t_out),
+                                       PermutationVector(piv_h, m), fc), dt)
 
 
 def ltlt_unb_ll(x: SkewMatrixLower, pivot=False, first_column=None) -> FactorizationResult:
@@ -129,7 +124,7 @@ def ltlt_unb_ll(x: SkewMatrixLower, pivot=False, first_column=None) -> Factoriza
     """
     if pivot and first_column is not None:
         raise ValueError("first_column is only supported without pivoting")
-    x, xd, on_device = _prep(x)
+    x, xd, on_device, dt = _prep(x)
     m = x.m
     fcvec = None
     if pivot:
@@ -142,7 +137,7 @@ def ltlt_unb_ll(x: SkewMatrixLower, pivot=False, first_column=None) -> Factoriza
         piv_h = np.zeros(0, dtype=np.int64)
     tau_h = tau.cpu().numpy()
     fc = flops_unb_ll(m, tau_h, piv_h if pivot else None, first_column=fcvec is not None)
-    return _result(L, tau_h, tau, piv_h, m, fc, on_device, fcvec)
+    return _result(L, tau_h, tau, piv_h, m, fc, on_device, fcvec, dt)
 
 
 def ltlt_unb_rl(x: SkewMatrixLower, pivot=False) -> FactorizationResult:
@@ -152,7 +147,7 @@ def ltlt_unb_rl(x: SkewMatrixLower, pivot=False) -> FactorizationResult:
     GPU computes them with the blocked left-looking-panel driver and reports
     the right-looking tally (instrument.flops_unb_rl).
     """
-    x, xd, on_device = _prep(x)
+    x, xd, on_device, dt = _prep(x)
     m = x.m
     if pivot:
         L, tau, piv = ltlt_blk_piv_device(xd, b=max(m, 1), fused="var1")
@@ -162,7 +157,7 @@ def ltlt_unb_rl(x: SkewMatrixLower, pivot=False) -> FactorizationResult:
         piv_h = np.zeros(0, dtype=np.int64)
     tau_h = tau.cpu().numpy()
     fc = flops_unb_rl(m, tau_h, piv_h if pivot else None)
-    return _result(L, tau_h, tau, piv_h, m, fc, on_device)
+    return _result(L, tau_h, tau, piv_h, m, fc, on_device, dt=dt)
 
 
 def ltlt_unb_panel(x: SkewMatrixLower, panel_width, variant="ll", pivot=False,
@@ -176,7 +171,7 @@ def ltlt_unb_panel(x: SkewMatrixLower, panel_width, variant="ll", pivot=False,
         raise InvalidVariant("a pivoted panel factorization must be left-looking")
     if pivot and first_column is not None:
         raise ValueError("first_column is only supported without pivoting")
-    x, xd, on_device = _prep(x)
+    x, xd, on_device, dt = _prep(x)
     m = x.m
     t = dv.require_cuda()
     fcvec = None
@@ -205,7 +200,7 @@ def ltlt_unb_panel(x: SkewMatrixLower, panel_width, variant="ll", pivot=False,
     piv_h = piv.cpu().numpy()[:nelim + 1] if pivot else np.zeros(0, dtype=np.int64)
     pfull = piv.cpu().numpy() if pivot else None
     fc = flops_unb_panel(m, int(panel_width), variant, tau_h, pfull, first_column=fcvec is not None)
-    return _result(L, tau_h, tau, piv_h, m, fc, on_device, fcvec)
+    return _result(L, tau_h, tau, piv_h, m, fc, on_device, fcvec, dt)
 
 
 __all__ = ["ltlt_unb_twostep", "ltlt_unb_twostep_device", "ltlt_unb_ll", "ltlt_unb_rl", "ltlt_unb_panel", "_is_torch"]
