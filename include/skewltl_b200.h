@@ -81,6 +81,11 @@ int skl_form_w(int n, int k, const double* A, long long lda, const double* tau, 
 int skl_skew_rank2_lower(int n, double alpha, const double* x, const double* y, double beta, double* A,
                          long long lda, void* stream);
 
+/* gen_rank2 (kernels2.py:134-163): A := beta*A + alpha*(x u^T + y v^T) on a p x q
+ * column-major rectangle (x, y length p; u, v length q) */
+int skl_gen_rank2(int p, int q, double alpha, const double* x, const double* u, const double* y, const double* v,
+                  double beta, double* A, long long lda, void* stream);
+
 /* skew_tridiag_gemv (kernels2.py:178-229):
  *   y := beta*y + alpha*(A (T x))[tail_from:], A is p x k, T = tridiag(tau[0..k-2]) */
 int skl_skew_tridiag_gemv(int p, int k, double alpha, const double* A, long long lda, const double* tau,

@@ -9,8 +9,8 @@ from .core import (InvalidVariant, PermutationVector, PivotUnsupported, Singular
                    SkewMatrixLower, SkewTridiagonal, SSplitting, UnitLowerFactor, ZeroPivot,
                    apply_symmetric_pivot, compose_permutation, form_s_splitting, invert_permutation,
                    pack_in_place, random_skew, reconstruct, unpack_in_place)
-from .instrument import FlopCounter  # noqa: F401
-from .blocked import (DEFAULT_BLOCK, FactorizationResult, Features, ltlt_blk_device,  # noqa: F401
+from .instrument import CallTrace, FlopCounter  # noqa: F401
+from .blocked import (DEFAULT_BLOCK, LADDER, FactorizationResult, Features, ltlt_blk_device,  # noqa: F401
                       ltlt_blk_left, ltlt_blk_piv, ltlt_blk_piv_device, ltlt_blk_piv_host, ltlt_blk_twostep,
                       ltlt_blk_var1, ltlt_blk_var2a, ltlt_blk_var2b)
 from .unblocked import ltlt_unb_ll, ltlt_unb_panel, ltlt_unb_rl, ltlt_unb_twostep  # noqa: F401

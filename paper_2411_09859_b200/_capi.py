@@ -33,6 +33,7 @@ SIGNATURES = {
     "skl_skew_tridiag_gemm_workspace_size": (_sz, [_i, _i, _i]),
     "skl_skew_tridiag_gemm": (_i, [_i, _i, _i, _d, _p, _ll, _p, _p, _ll, _d, _p, _ll, _i, _p, _sz, _p]),
     "skl_skew_rank2_lower": (_i, [_i, _d, _p, _p, _d, _p, _ll, _p]),
+    "skl_gen_rank2": (_i, [_i, _i, _d, _p, _p, _p, _p, _d, _p, _ll, _p]),
     "skl_skew_tridiag_gemv": (_i, [_i, _i, _d, _p, _ll, _p, _p, _d, _p, _i, _p]),
     "skl_apply_row_pivots_workspace_size": (_sz, [_i, _i, _i]),
     "skl_apply_row_pivots": (_i, [_i, _i, _p, _ll, _p, _i, _i, _p, _sz, _p]),

@@ -34,6 +34,23 @@ class Features:
     external_t: bool = True
     fused_l3: bool = True
 
+    @property
+    def l2_workers(self):
+        return None if self.parallel_l2 else 1
+
+
+#: optimisation ladder (blocked.py:67-75): cumulative CPU feature steps, accepted
+#: by every driver; the GPU kernels are the same at every step
+LADDER = {
+    "step0": Features(fused_l2=False, parallel_l2=False, external_t=False, fused_l3=False),
+    "step1": Features(fused_l2=True, parallel_l2=False, external_t=False, fused_l3=False),
+    "step2": Features(fused_l2=True, parallel_l2=True, external_t=False, fused_l3=False),
+    "step3": Features(fused_l2=True, parallel_l2=True, external_t=True, fused_l3=False),
+    "step4": Features(fused_l2=True, parallel_l2=True, external_t=True, fused_l3=True),
+    "step5": Features(fused_l2=True, parallel_l2=True, external_t=True, fused_l3=True),
+}
+LADDER_VARIANT = {name: ("blk-var2b" if name == "step5" else "blk-var1") for name in LADDER}
+
 
 @dataclass
 class FactorizationResult:

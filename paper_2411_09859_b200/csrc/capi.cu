@@ -479,6 +479,15 @@ int skl_skew_rank2_lower(int n, double alpha, const double* x, const double* y, 
   return SKL_OK;
 }
 
+int skl_gen_rank2(int p, int q, double alpha, const double* x, const double* u, const double* y, const double* v,
+                  double beta, double* A, long long lda, void* stream) {
+  if (p < 0 || q < 0 || (p > 0 && q > 0 && lda < p)) return SKL_BAD_ARGUMENT;
+  if (p == 0 || q == 0 || (alpha == 0.0 && beta == 1.0)) return SKL_OK;
+  SKL_TRY(skl::launch_gen_rank2(A, lda, p, q, alpha, x, u, y, v, beta, static_cast<cudaStream_t>(stream)));
+  g_kt.launches++;
+  return SKL_OK;
+}
+
 int skl_skew_tridiag_gemv(int p, int k, double alpha, const double* A, long long lda, const double* tau,
                           const double* x, double beta, double* y, int tail_from, void* stream) {
   if (p < 0 || k < 0 || tail_from < 0 || tail_from > p || (p > 0 && lda < p)) return SKL_BAD_ARGUMENT;

@@ -75,6 +75,8 @@ cudaError_t launch_form_w(const double* A, long long lda, int n, int k, const do
 // ---- level-2 kernels ------------------------------------------------------
 cudaError_t launch_skew_rank2(double* A, long long lda, int n, double alpha, const double* x, const double* y,
                               double beta, cudaStream_t stream);
+cudaError_t launch_gen_rank2(double* A, long long lda, int p, int q, double alpha, const double* x,
+                            const double* u, const double* y, const double* v, double beta, cudaStream_t stream);
 cudaError_t launch_skew_tridiag_gemv(double* y, double alpha, const double* A, long long lda, int p, int k,
                                      const double* tau, const double* x, double beta, int tail_from,
                                      cudaStream_t stream);

@@ -1,5 +1,6 @@
 // Level-2 kernels behind the reference's kernels2.py API.
 //   skew_rank2         kernels2.py:93-131   A_lower := beta A + alpha (x y^T - y x^T)
+//   gen_rank2          kernels2.py:134-163  A := beta A + alpha (x u^T + y v^T), p x q rectangle
 //   skew_tridiag_gemv  kernels2.py:178-229  y := beta y + alpha (A (T x))[tail_from:]
 //   apply_row_pivots   kernels2.py:232-271  rows [lo, hi) := rows idx[lo:hi] (one gather)
 //   _sym_swap_lower    core.py:294-324      X := P X P^T for one transposition
@@ -20,6 +21,20 @@ __global__ void skew_rank2_kernel(double* __restrict__ A, long long lda, int n, 
       double* p = A + (long long)j * lda + i;
       double upd = alpha * (x[i] * yj - y[i] * xj);
       *p = (beta == 1.0) ? *p + upd : beta * *p + upd;
+    }
+  }
+}
+
+// general rank-2 on a p x q column-major rectangle (HBM-bound: one read + one write per entry)
+__global__ void gen_rank2_kernel(double* __restrict__ A, long long lda, int p, int q, double alpha,
+                                 const double* __restrict__ x, const double* __restrict__ u,
+                                 const double* __restrict__ y, const double* __restrict__ v, double beta) {
+  for (int j = blockIdx.y; j < q; j += gridDim.y) {
+    const double uj = alpha * u[j], vj = alpha * v[j];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p; i += gridDim.x * blockDim.x) {
+      double* e = A + (long long)j * lda + i;
+      const double upd = fma(x[i], uj, y[i] * vj);
+      *e = (beta == 1.0) ? *e + upd : fma(beta, *e, upd);
     }
   }
 }
@@ -144,6 +159,13 @@ cudaError_t launch_skew_rank2(double* A, long long lda, int n, double alpha, con
                               double beta, cudaStream_t stream) {
   if (n <= 1) return cudaSuccess;
   skew_rank2_kernel<<<col_grid(n, n), 256, 0, stream>>>(A, lda, n, alpha, x, y, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gen_rank2(double* A, long long lda, int p, int q, double alpha, const double* x,
+                            const double* u, const double* y, const double* v, double beta, cudaStream_t stream) {
+  if (p <= 0 || q <= 0) return cudaSuccess;
+  gen_rank2_kernel<<<col_grid(p, q), 256, 0, stream>>>(A, lda, p, q, alpha, x, u, y, v, beta);
   return cudaGetLastError();
 }
 

@@ -18,7 +18,8 @@ reference's accounting rules exactly:
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from contextlib import contextmanager
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -39,6 +40,82 @@ class FlopCounter:
     def __add__(self, other: "FlopCounter") -> "FlopCounter":
         return FlopCounter(self.level2 + other.level2, self.level3 + other.level3,
                            self.panel + other.panel, self.pivot + other.pivot)
+
+
+@dataclass
+class CallTrace:
+    """Chronological (kernel, scope) record of the reference's kernel calls
+    (instrument.py:44-54).  The GPU drivers run fused kernels, so the trace a
+    driver emits is the reference's call sequence replayed from the same
+    schedule and the returned pivots / tau (like the flop tallies below)."""
+
+    calls: list = field(default_factory=list)
+
+    def count(self, kernel=None, scope=None):
+        return sum(1 for k, s in self.calls if (kernel is None or k == kernel) and (scope is None or s == scope))
+
+
+# module-global accounting state, caller-serialised like the reference's (instrument.py:57-59)
+_counter = None
+_trace = None
+_scope = "trailing"
+
+
+@contextmanager
+def counting(counter):
+    """Route the tallies of the drivers called inside into ``counter`` (instrument.py:62-71)."""
+    global _counter
+    saved, _counter = _counter, counter
+    try:
+        yield counter
+    finally:
+        _counter = saved
+
+
+@contextmanager
+def tracing(trace):
+    """Record the (replayed) kernel calls of the drivers called inside (instrument.py:74-84)."""
+    global _trace
+    saved, _trace = _trace, trace
+    try:
+        yield trace
+    finally:
+        _trace = saved
+
+
+@contextmanager
+def scope(name):
+    global _scope
+    saved, _scope = _scope, name
+    try:
+        yield
+    finally:
+        _scope = saved
+
+
+def current_scope():
+    return _scope
+
+
+def add_flops(kind, n):
+    """instrument.py:101-113: adds to the active counter (if any)."""
+    if _counter is not None:
+        setattr(_counter, kind, getattr(_counter, kind) + int(n))
+
+
+def record_call(kernel):
+    if _trace is not None:
+        _trace.calls.append((kernel, _scope))
+
+
+def _emit(fc, calls):
+    """Hand a replayed driver's tally and call sequence to the active counter / trace."""
+    if _counter is not None:
+        for kind in ("level2", "level3", "panel", "pivot"):
+            add_flops(kind, getattr(fc, kind))
+    if _trace is not None:
+        _trace.calls.extend(calls)
+    return fc
 
 
 def _lower(n):
@@ -85,6 +162,8 @@ def reference_schedule(m, b, fused):
 def flops_blk_piv(m, b, fused, pivots, tau):
     """FlopCounter of ltlt_blk_piv(x, b, fused) given its pivots and tau."""
     fc = FlopCounter()
+    calls = []
+    outer = _scope
     pivots = np.asarray(pivots)
     tau = np.asarray(tau)
     for r, nelim, lo, c0 in reference_schedule(m, b, fused):
@@ -93,6 +172,7 @@ def flops_blk_piv(m, b, fused, pivots, tau):
             if k >= 2:
                 rows = m - g - 1
                 fc.panel += 2 * rows * k + 4 * k
+                calls.append(("skew_tridiag_gemv", "panel"))
             off = int(pivots[g + 1])
             if off:
                 a = g + 1 - lo
@@ -103,20 +183,25 @@ def flops_blk_piv(m, b, fused, pivots, tau):
             sub = pivots[r + 1:r + nelim + 1]
             if np.any(sub):
                 fc.pivot += _row_pivot_moves(m - r - 1, sub) * lo
+                calls.append(("apply_row_pivots", outer))
         rt = r + nelim
         if m - rt >= 2 and rt - c0 >= 1:
             n = m - rt
             k = rt - c0 + 1
             fc.level3 += 2 * k * _lower(n) + 4 * k * n
+            calls.append(("skew_tridiag_rankk", outer))
         if fused == "var1" and m - rt >= 2:
             n = m - rt - 1
             fc.level2 += 2 * n * max(n - 1, 0)
-    return fc
+            calls.append(("skew_rank2", outer))
+    return _emit(fc, calls)
 
 
 def flops_unb_twostep(m, pivots, tau, pivot=True):
     """FlopCounter of ltlt_unb_twostep (unblocked.py:136-171,229-240)."""
     fc = FlopCounter()
+    calls = []
+    outer = _scope
     pivots = np.asarray(pivots)
     tau = np.asarray(tau)
 
@@ -132,6 +217,7 @@ def flops_unb_twostep(m, pivots, tau, pivot=True):
         nsq = m - start
         if nsq > 0:
             fc.level2 += 2 * nsq * max(nsq - 1, 0)
+            calls.append(("skew_rank2", outer))
 
     end = m - 1
     g = 0
@@ -148,7 +234,7 @@ def flops_unb_twostep(m, pivots, tau, pivot=True):
             fc.level2 += 6 * max(m - s, 0)
             skr2(s)
         g += 2
-    return fc
+    return _emit(fc, calls)
 
 
 def flop_model(variant, m, b=None):
@@ -169,6 +255,14 @@ class _Tally:
     def __init__(self):
         self.fc = FlopCounter()
         self.in_panel = False
+        self.calls = []
+        self.outer = _scope
+
+    def call(self, kernel):
+        self.calls.append((kernel, "panel" if self.in_panel else self.outer))
+
+    def done(self):
+        return _emit(self.fc, self.calls)
 
     def add(self, kind, n):
         n = int(n)
@@ -191,6 +285,7 @@ def _t_elim(t, m, g, tau, pivots=None, swap_from=0):
 
 def _t_skew_rank2(t, n):
     """skew_rank2 (kernels2.py:93-131)."""
+    t.call("skew_rank2")
     t.add("level2", 2 * n * max(n - 1, 0))
 
 
@@ -202,6 +297,7 @@ def _t_trapezoid(t, m, start, climit):
         return
     _t_skew_rank2(t, nsq)
     if climit < m:
+        t.call("gen_rank2")
         t.add("level2", 4 * (m - climit) * nsq)
 
 
@@ -211,6 +307,7 @@ def _t_panel_ll(t, m, tau, base, nelim, lo, pivots=None, swap_from=None):
     for g in range(base, base + nelim):
         k = g - lo
         if k >= 2:
+            t.call("skew_tridiag_gemv")
             t.add("level2", 2 * (m - g - 1) * k + 4 * k)
         _t_elim(t, m, g, tau, pivots, swap_from)
 
@@ -262,6 +359,7 @@ def _t_run_panel(t, m, tau, base, nelim, variant, carry):
 
 def _t_rankk(t, n, k):
     """skew_tridiag_rankk (kernels3.py:164)."""
+    t.call("skew_tridiag_rankk")
     t.add("level3", 2 * k * _lower(n) + 4 * k * n)
 
 
@@ -308,6 +406,7 @@ def flops_blk_unpivoted(m, b, driver, panel_variant, tau, work=None):
             if r >= 2:   # skew_tridiag_gemm(tril) (kernels3.py:239-259): p = m-r, q = be, k = r
                 p, q, k = m - r, be, r
                 written = _lower(min(p, q)) + max(p - q, 0) * q
+                t.call("skew_tridiag_gemm")
                 t.add("level3", 2 * k * written + 4 * k * q)
             _t_run_panel(t, m, tau, r, be, panel_variant, r > 0)
             r += be
@@ -323,7 +422,9 @@ def flops_blk_unpivoted(m, b, driver, panel_variant, tau, work=None):
                 n, k = m - rt, rt - c0 + 1
                 if driver == "twostep":
                     a = np.asarray(work)[rt:, c0 - 1:rt]
+                    t.call("form_w")
                     t.add("level3", 2 * n * _s_entries(k))              # form_w (kernels3.py:364)
+                    t.call("skew_rank2k")
                     t.add("level3", 4 * rank2k_keff(a, tau[c0:rt]) * _lower(n))
                 else:
                     _t_rankk(t, n, k)
@@ -331,14 +432,14 @@ def flops_blk_unpivoted(m, b, driver, panel_variant, tau, work=None):
                 _t_skew_rank2(t, m - rt - 1)
             pending = True
             r = rt
-    return t.fc
+    return t.done()
 
 
 def flops_unb_rl(m, tau, pivots=None):
     """FlopCounter of ltlt_unb_rl (unblocked.py:192-202)."""
     t = _Tally()
     _t_panel_rl(t, m, np.asarray(tau), 0, m - 1, m, pivots, 0)
-    return t.fc
+    return t.done()
 
 
 def flops_unb_ll(m, tau, pivots=None, first_column=False):
@@ -347,7 +448,7 @@ def flops_unb_ll(m, tau, pivots=None, first_column=False):
     if first_column:
         _t_skew_rank2(t, m - 1)
     _t_panel_ll(t, m, np.asarray(tau), 0, m - 1, 0, pivots, 0)
-    return t.fc
+    return t.done()
 
 
 def flops_unb_panel(m, width, variant, tau, pivots=None, first_column=False):
@@ -366,4 +467,4 @@ def flops_unb_panel(m, width, variant, tau, pivots=None, first_column=False):
     else:
         _t_panel_twostep(t, m, tau, 0, nelim, climit)
     t.in_panel = False
-    return t.fc
+    return t.done()

@@ -1,18 +1,24 @@
 """Level-2 kernels (drop-in for reference ``kernels2.py``).
 
-``skew_rank2`` (kernels2.py:93-131), ``skew_tridiag_gemv`` (kernels2.py:178-229)
-and ``apply_row_pivots`` (kernels2.py:232-271) with the reference's
-signatures and in-place semantics; the arithmetic runs in the CUDA library.
-NumPy operands are staged to the GPU and the output view written back;
-column-major torch CUDA tensors are updated in place.
+``skew_rank2`` (kernels2.py:93-131), ``gen_rank2`` (kernels2.py:134-163),
+``skew_tridiag_gemv`` (kernels2.py:178-229), ``apply_row_pivots``
+(kernels2.py:232-271) and ``trapezoid_rank2`` / ``PanelView``
+(kernels2.py:274-312) with the reference's signatures and in-place
+semantics; the arithmetic runs in the CUDA library.  NumPy operands are
+staged to the GPU and the output view written back; column-major torch CUDA
+tensors are updated in place.  Every call is recorded in the active
+``instrument`` trace / counter with the reference's flop rule.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
+from dataclasses import dataclass
+
 from . import _capi
 from . import device as dv
+from . import instrument
 from .core import SkewTridiagonal, _is_torch
 
 JAM = 64                 # kernels2.py:24 (CPU column jamming; informational)
@@ -44,6 +50,8 @@ def skew_rank2(a, alpha, x, y, beta=1, workers=None):
     n = a.shape[0]
     if a.shape[1] != n or len(x) != n or len(y) != n:
         raise ValueError("dimension mismatch")
+    instrument.record_call("skew_rank2")
+    instrument.add_flops("level2", 2 * n * max(n - 1, 0))
     if n <= 1 or (alpha == 0 and beta == 1):
         return
     dv.require_cuda()
@@ -53,6 +61,58 @@ def skew_rank2(a, alpha, x, y, beta=1, workers=None):
     _capi.check(st, "skew_rank2")
     if not _is_torch(a):
         a[...] = dv.to_host_colmajor(ad)
+
+
+def gen_rank2(a, alpha, x, u, y, v, beta=1, workers=None, fused=True):
+    """A := beta A + alpha (x u^T + y v^T) on a p x q rectangle (kernels2.py:134-163).
+    ``fused`` / ``workers`` are accepted for compatibility: one pass on the GPU."""
+    p, q = a.shape
+    if len(x) != p or len(y) != p or len(u) != q or len(v) != q:
+        raise ValueError("dimension mismatch")
+    instrument.record_call("gen_rank2")
+    instrument.add_flops("level2", 4 * p * q)
+    if p == 0 or q == 0 or (alpha == 0 and beta == 1):
+        return
+    dv.require_cuda()
+    ad = _mat(a)
+    xd, ud, yd, vd = _vec(x), _vec(u), _vec(y), _vec(v)
+    st = _capi.load().skl_gen_rank2(p, q, float(alpha), xd.data_ptr(), ud.data_ptr(), yd.data_ptr(), vd.data_ptr(),
+                                    float(beta), ad.data_ptr(), dv.ld_of(ad), dv.stream_ptr())
+    _capi.check(st, "gen_rank2")
+    if not _is_torch(a):
+        a[...] = dv.to_host_colmajor(ad)
+
+
+@dataclass
+class PanelView:
+    """Trapezoidal update region [start, n) x [start, climit) of a lower-stored
+    skew matrix (kernels2.py:274-293): a square skew part plus the rectangle below."""
+
+    buf: object
+    start: int
+    climit: int
+
+    @property
+    def square(self):
+        return self.buf[self.start:self.climit, self.start:self.climit]
+
+    @property
+    def rect(self):
+        return self.buf[self.climit:, self.start:self.climit]
+
+
+def trapezoid_rank2(buf, start, climit, alpha, x, y, workers=None, fused=True):
+    """alpha (x y^T - y x^T) on rows/cols [start, n) of ``buf``, columns < climit
+    (kernels2.py:296-312): skew_rank2 on the square + gen_rank2 on the rectangle."""
+    n = buf.shape[0]
+    climit = min(climit, n)
+    nsq = climit - start
+    if nsq <= 0:
+        return
+    view = PanelView(buf, start, climit)
+    skew_rank2(view.square, alpha, x[:nsq], y[:nsq], 1, workers=workers)
+    if climit < n:
+        gen_rank2(view.rect, alpha, x[nsq:], y[:nsq], -y[nsq:], x[:nsq], 1, workers=workers, fused=fused)
 
 
 def tridiag_matvec(tau, x):
@@ -75,6 +135,8 @@ def skew_tridiag_gemv(y, alpha, a, t: SkewTridiagonal, x, beta=1, workers=None, 
     rows = p - tail_from
     if t.m != k or len(x) != k or len(y) != rows or rows < 0:
         raise ValueError("dimension mismatch")
+    instrument.record_call("skew_tridiag_gemv")
+    instrument.add_flops("level2", 2 * rows * k + 4 * k)
     if rows == 0:
         return
     dv.require_cuda()
@@ -108,6 +170,8 @@ def apply_row_pivots(block, p, forward=True, workers=None):
         inv[idx] = np.arange(n)
         idx = inv
     moved = idx != np.arange(n)
+    instrument.record_call("apply_row_pivots")
+    instrument.add_flops("pivot", int(np.count_nonzero(moved)) * q)
     if not moved.any() or q == 0:
         return
     touched = np.flatnonzero(moved)

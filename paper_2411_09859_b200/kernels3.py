@@ -5,16 +5,48 @@ Same signatures and in-place semantics as the reference:
 (kernels3.py:151-209), ``skew_tridiag_gemm`` (kernels3.py:239-302),
 ``form_w`` (kernels3.py:354-364).  Operands may be
 NumPy arrays (copied to the GPU and the output view written back) or
-column-major torch CUDA tensors (updated in place on the device).
+column-major torch CUDA tensors (updated in place on the device).  Every
+call is recorded in the active ``instrument`` trace / counter with the
+reference's flop rule.
 """
 
 from __future__ import annotations
+
+from dataclasses import dataclass, replace
 
 import numpy as np
 
 from . import _capi
 from . import device as dv
+from . import instrument
 from .core import SkewTridiagonal, SSplitting, _is_torch
+
+
+@dataclass(frozen=True)
+class BlockConfig:
+    """CPU cache-blocking constants (kernels3.py:28-41), kept for compatibility:
+    the GPU tiles are fixed by the kernels (128x128 DMMA tiles), so these only
+    round-trip through set_block_config / get_block_config."""
+
+    m_c: int = 128
+    k_c: int = 256
+    n_c: int = 256
+    m_r: int = 8
+    n_r: int = 4
+
+
+_config = BlockConfig()
+
+
+def set_block_config(**kw):
+    global _config
+    _config = replace(_config, **kw)
+    return _config
+
+
+def get_block_config() -> BlockConfig:
+    return _config
+
 
 last_keff = 0
 
@@ -45,6 +77,7 @@ def skew_rank2k(c, alpha, a, b, beta=1, *, workers=None, skip_zero_columns=True)
         raise ValueError("dimension mismatch")
     _check_alias(c, a, "a")
     _check_alias(c, b, "b")
+    instrument.record_call("skew_rank2k")
     t = dv.require_cuda()
     cd, ad, bd = _dev(c), _dev(a), _dev(b)
     lib = _capi.load()
@@ -57,6 +90,7 @@ def skew_rank2k(c, alpha, a, b, beta=1, *, workers=None, skip_zero_columns=True)
     _capi.check(st, "skew_rank2k")
     _writeback(c, cd)
     last_keff = int(keff.item())
+    instrument.add_flops("level3", 4 * last_keff * (n * (n - 1) // 2))
     return None
 
 
@@ -66,6 +100,8 @@ def skew_tridiag_rankk(c, alpha, a, t: SkewTridiagonal, beta=1, *, fused=True, w
     if c.shape[0] != n or c.shape[1] != n or t.m != k:
         raise ValueError("dimension mismatch")
     _check_alias(c, a, "a")
+    instrument.record_call("skew_tridiag_rankk")
+    instrument.add_flops("level3", 2 * k * (n * (n - 1) // 2) + 4 * k * n)
     tt = dv.require_cuda()
     cd, ad = _dev(c), _dev(a)
     tau = t.tau if _is_torch(t.tau) else dv.vec_to_device(np.asarray(t.tau, dtype=np.float64), tt.float64)
@@ -91,6 +127,9 @@ def skew_tridiag_gemm(c, alpha, a, t: SkewTridiagonal, b, beta=1, *, tril=False,
         raise ValueError("dimension mismatch")
     _check_alias(c, a, "a")
     _check_alias(c, b, "b")
+    instrument.record_call("skew_tridiag_gemm")
+    written = (min(p, q) * (min(p, q) - 1) // 2 + max(p - q, 0) * q) if tril else p * q
+    instrument.add_flops("level3", 2 * k * written + 4 * k * q)
     tt = dv.require_cuda()
     cd, ad, bd = _dev(c), _dev(a), _dev(b)
     tau = t.tau if _is_torch(t.tau) else dv.vec_to_device(np.asarray(t.tau, dtype=np.float64), tt.float64)
@@ -111,6 +150,8 @@ def form_w(a, s):
     n, kdim = a.shape
     if s.m != kdim:
         raise ValueError("dimension mismatch")
+    instrument.record_call("form_w")
+    instrument.add_flops("level3", 2 * n * len(s.entries))
     tt = dv.require_cuda()
     # recover tau from the splitting (core.py:153-169 pattern)
     tau = np.zeros(max(kdim - 1, 0), dtype=np.float64)

@@ -187,3 +187,70 @@ def test_skew_tridiag_gemm_device_tensors_and_alias():
     with pytest.raises(ValueError):
         k3().skew_tridiag_gemm(np.zeros((5, 4)), 1.0, np.zeros((5, 3)), SkewTridiagonal(np.ones(2)),
                                np.zeros((3, 5)))
+
+
+# ---- gen_rank2 / trapezoid_rank2 (kernels2.py:134-163, 274-312) -----------------
+
+def test_gen_rank2_scalar_and_dense():
+    from paper_2411_09859_b200 import instrument as ins
+    from paper_2411_09859_b200.kernels2 import gen_rank2
+    a = np.array([[2.0]])
+    gen_rank2(a, 0.5, np.array([3.0]), np.array([4.0]), np.array([5.0]), np.array([6.0]), 1.0)
+    assert a[0, 0] == 2.0 + 0.5 * (12.0 + 30.0)
+    rng = np.random.default_rng(3)
+    for p, q, beta in ((8, 4, 0.25), (1000, 37, 1.0), (3, 1, -1.0)):
+        a = np.asfortranarray(rng.standard_normal((p, q)))
+        x, y, u, v = rng.standard_normal(p), rng.standard_normal(p), rng.standard_normal(q), rng.standard_normal(q)
+        want = beta * a + 2.0 * (np.outer(x, u) + np.outer(y, v))
+        tr, fc = ins.CallTrace(), ins.FlopCounter()
+        with ins.tracing(tr), ins.counting(fc):
+            gen_rank2(a, 2.0, x, u, y, v, beta)
+        assert np.allclose(a, want, rtol=1e-14, atol=1e-14)
+        assert tr.calls == [("gen_rank2", "trailing")] and fc.level2 == 4 * p * q
+    a = rng.standard_normal((4, 3))
+    before = a.copy()
+    gen_rank2(a, 0.0, np.ones(4), np.ones(3), np.ones(4), np.ones(3), 1.0)
+    assert np.array_equal(a, before)
+    with pytest.raises(ValueError):
+        gen_rank2(a, 1.0, np.ones(3), np.ones(3), np.ones(4), np.ones(3), 1.0)
+
+
+def test_trapezoid_rank2_matches_dense():
+    from paper_2411_09859_b200.kernels2 import trapezoid_rank2
+    rng = np.random.default_rng(4)
+    for n, start, climit in ((10, 3, 7), (300, 20, 140), (50, 5, 50)):
+        buf = np.asfortranarray(rng.standard_normal((n, n)))
+        x, y = rng.standard_normal(n - start), rng.standard_normal(n - start)
+        want = buf.copy()
+        full = np.zeros((n, n))
+        full[start:, start:] = np.outer(x, y) - np.outer(y, x)
+        il, jl = np.tril_indices(n, -1)
+        keep = (jl >= start) & (jl < climit)
+        want[il[keep], jl[keep]] += full[il[keep], jl[keep]]
+        trapezoid_rank2(buf, start, climit, 1.0, x, y)
+        assert np.allclose(np.tril(buf, -1), np.tril(want, -1), rtol=1e-13, atol=1e-13)
+        assert np.array_equal(np.triu(buf), np.triu(want))
+    buf = np.asfortranarray(rng.standard_normal((4, 4)))
+    before = buf.copy()
+    trapezoid_rank2(buf, 3, 3, 1.0, np.ones(1), np.ones(1))
+    assert np.array_equal(buf, before)
+
+
+def test_kernel_wrappers_record_reference_calls():
+    from paper_2411_09859_b200 import instrument as ins
+    from paper_2411_09859_b200.core import SkewTridiagonal
+    from paper_2411_09859_b200.kernels2 import skew_rank2, skew_tridiag_gemv
+    from paper_2411_09859_b200.kernels3 import skew_tridiag_rankk
+    rng = np.random.default_rng(5)
+    n, k = 40, 6
+    c = np.asfortranarray(rng.standard_normal((n, n)))
+    a = np.asfortranarray(rng.standard_normal((n, k)))
+    t = SkewTridiagonal(rng.standard_normal(k - 1))
+    tr, fc = ins.CallTrace(), ins.FlopCounter()
+    with ins.tracing(tr), ins.counting(fc), ins.scope("panel"):
+        skew_rank2(c, 1.0, rng.standard_normal(n), rng.standard_normal(n))
+        skew_tridiag_gemv(np.zeros(n - 5), -1.0, a, t, rng.standard_normal(k), 1.0, tail_from=5)
+        skew_tridiag_rankk(c, -1.0, a, t, 1.0)
+    assert tr.calls == [("skew_rank2", "panel"), ("skew_tridiag_gemv", "panel"), ("skew_tridiag_rankk", "panel")]
+    assert fc.level2 == 2 * n * (n - 1) + 2 * (n - 5) * k + 4 * k
+    assert fc.level3 == 2 * k * (n * (n - 1) // 2) + 4 * k * n

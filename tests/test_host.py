@@ -109,3 +109,18 @@ def test_reference_schedule_shapes():
     assert len(s) == 32 and s[0] == (0, 128, 0, 1) and s[-1][0] + s[-1][1] == 4095
     s2 = reference_schedule(1000, 100, "var2b")
     assert s2[0][1] == 101 and s2[1][2] == 100
+
+
+def test_panel_view_shapes_and_block_config_roundtrip():
+    import numpy as np
+    from paper_2411_09859_b200.kernels2 import PanelView
+    from paper_2411_09859_b200.kernels3 import get_block_config, set_block_config
+    v = PanelView(np.zeros((8, 8), order="F"), 2, 5)
+    assert v.square.shape == (3, 3) and v.rect.shape == (3, 3)
+    saved = get_block_config()
+    try:
+        assert set_block_config(m_c=16, k_c=8).k_c == 8 and get_block_config().m_c == 16
+    finally:
+        set_block_config(m_c=saved.m_c, k_c=saved.k_c, n_c=saved.n_c)
+    import paper_2411_09859_b200 as pk
+    assert set(pk.LADDER) == {f"step{i}" for i in range(6)} and pk.LADDER["step0"].l2_workers == 1
