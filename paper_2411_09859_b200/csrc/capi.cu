@@ -114,6 +114,13 @@ int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
+// single-cluster pivoted panel: candidate rows pushed through DSMEM with lazy
+// interchanges (panel_cluster.cu, push mode); SKL_PANEL_PUSH=0 keeps the L2 row exchange
+bool panel_push() {
+  static int on = env_int("SKL_PANEL_PUSH", 1);
+  return on != 0;
+}
+
 bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int rows = n - (lo + 1);
   // GPU panel width cap for the cluster panel (per-step cost grows with the width while the
@@ -133,10 +140,11 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
     if (C > Cmax) C = Cmax;
     int Rc = (rows + C - 1) / C;
     if (Rc <= 1024) {
-      int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
-      while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo) > smem_limit()) --w;
       static int min_w = env_int("SKL_MIN_CLUSTER_W", 64);
       static int ll_single = env_int("SKL_LL_SINGLE", 1);
+      const int npush = (ll_single && panel_push()) ? C : 0;  // room for the pushed candidate rows
+      int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
+      while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo, npush) > smem_limit()) --w;
       if (w >= 1 && w >= std::min(want, min_w)) {
         // default (SKL_LL_SINGLE=1): the one cluster runs the multi-cluster kernel with
         // Q = 1 -- st.async candidate all-to-all + flagged pivot rows through L2, no
@@ -656,6 +664,7 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
     a.prof = g_prof;
     a.pivot = pivot;
     a.info = info;
+    a.push = (p.cluster == 2 && p.ctas == p.csize && pivot && panel_push()) ? 1 : 0;
     {
       KScope ks(KPANEL, st);
       if (p.cluster == 2)

@@ -115,6 +115,7 @@ struct PanelArgs {
   unsigned long long* prof;  // optional per-CTA phase cycle totals [C][16]
   int pivot;             // 0: unpivoted (pivot row = row g+1), exact-zero breakdown -> *info
   int* info;             // device: first breaking column + 1 (0 = none); may be null when pivot
+  int push;              // single-cluster pivoted panel: candidate rows pushed by st.async, lazy interchanges
 };
 size_t panel_smem_bytes(int rows_per, int kmax);
 int panel_max_ctas();
@@ -122,7 +123,7 @@ int panel_threads();
 cudaError_t launch_panel(const PanelArgs& a, cudaStream_t stream);
 // single-cluster variant (DSMEM exchange); cluster size 16 (or 8), 0 if unavailable
 int panel_cluster_size();
-size_t panel_cluster_smem_bytes(int rows_per, int kmax);
+size_t panel_cluster_smem_bytes(int rows_per, int kmax, int npush = 0);
 cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
 // multi-cluster variant (cooperative; intra-cluster DSMEM + inter-cluster LL exchange)
 int panel_multi_clusters(int csize, size_t smem);

@@ -74,6 +74,17 @@ __device__ __forceinline__ void st_async_cand(CCand* slot_local, uint64_t* bar_l
                : "memory");
 }
 
+// two doubles -> the same smem offset in CTA `rank`, completing 16 bytes on its mbarrier
+__device__ __forceinline__ void st_async_f64x2(double* dst_local, uint64_t* bar_local, uint32_t rank, double x,
+                                               double y) {
+  uint32_t rdst, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(dst_local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(bar_local)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(rdst),
+               "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
+
 __device__ __forceinline__ void cluster_arrive_release() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
 }
@@ -114,11 +125,15 @@ struct CSmem {
   int* pivbuf;     // [nelim] pivot offsets of this panel (flushed at the end)
   CCand* gwin;     // [2] global winner (MULTI)
   uint64_t* xbar;  // MULTI: [0..1] candidate all-to-all, [2..3] global-winner delivery (st.async)
+  int* lab;        // [Rs] final position of each slab row (written after the step loop)
+  double* crows;   // push mode: [2][C][crow_stride(kmax)] candidate rows pushed by every CTA
 };
+
+__host__ __device__ inline int crow_stride(int kmax) { return (kmax + 3) & ~1; }  // even: 16-byte rows
 
 __host__ __device__ inline int cslab_stride(int rows_per) { return rows_per | 1; }
 
-__host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsigned char* base) {
+__host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsigned char* base, int npush = 0) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -162,6 +177,10 @@ __host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsign
   if (s) s->gwin = (CCand*)p;
   p = take(sizeof(uint64_t) * 4);
   if (s) s->xbar = (uint64_t*)p;
+  p = take(sizeof(int) * Rs);
+  if (s) s->lab = (int*)p;
+  p = take(sizeof(double) * 2 * (size_t)npush * crow_stride(kmax));
+  if (s) s->crows = (double*)p;
   return off;
 }
 
@@ -236,7 +255,14 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   const int rt = r + nelim;
 
   CSmem s;
-  csmem_layout(R, kmax, &s, smem_raw);
+  // push mode (one cluster, pivoted): every CTA pushes its candidate's row to every CTA
+  // with st.async next to the candidate, and symmetric interchanges are LAZY -- a slab row
+  // keeps its data and carries its position as a label (lab[]), so no row ever moves
+  // between CTAs and no pivot row is fetched through L2
+  const bool push = MULTI && Q == 1 && a.pivot && a.push;
+  csmem_layout(R, kmax, &s, smem_raw, push ? C : 0);
+  const int CRS = crow_stride(kmax);
+  const bool spread_pub = a.dbg & 64 ? false : true;  // dbg bit 6: the warp-0 publication (A/B)
   if (MULTI && tid == 0) {
     for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);  // one local arrival (expect_tx) per phase
     fence_mbar_init();  // made visible to the cluster by the cluster barrier below
@@ -263,8 +289,13 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   }
   cluster_barrier();
   long long pt[6] = {0, 0, 0, 0, 0, 0};
+  long long sub[3] = {0, 0, 0};  // phase-3 split (profiling only): winner | gathers issued | row poll done
   long long t_prev = clock64();
   const long long t_loop0 = t_prev;
+#define SUBMARK(i)                  \
+  do {                              \
+    sub[i] += clock64() - t_prev;   \
+  } while (0)
 #define CMARK(i)                    \
   do {                              \
     long long _t = clock64();       \
@@ -279,6 +310,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   // per-thread rows: li = tid + u * kCThreads (R <= 2 * kCThreads)
   double cnext[2] = {0.0, 0.0};
   bool cneg[2] = {false, false};  // gathered from the row part: negate at use (keeps the load in flight)
+  int lab[2] = {rbase + tid, rbase + tid + kCThreads};  // position of row li = tid + u * kCThreads
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int li = tid + u * kCThreads;
@@ -297,37 +329,43 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 
     if (MULTI && tid == 0) {
       // this step's deliveries: C candidates (16 B each) and the global winner (16 B)
-      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C) * sizeof(CCand));
+      const uint32_t rowb = push ? 16u * uint32_t((k + 2) >> 1) : 0u;
+      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C) * (uint32_t(sizeof(CCand)) + rowb));
       if (Q > 1) mbar_arrive_expect_tx(&s.xbar[2 + par], sizeof(CCand));
     }
 
     // ---- (1) v = c - A z; per-warp argmax -----------------------------------
     double vbest = 0.0;
-    int ibest = -1;
+    int ibest = -1, lbest = 0;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int li = tid + u * kCThreads;
-      const int pos = rbase + li;
+      const int pos = lab[u];
       if (li < rcount && pos > g) {
         const double v = (cneg[u] ? -cnext[u] : cnext[u]) - s.az[li];
         col[li] = v;
         if (ibest < 0 || fabs(v) > fabs(vbest)) {
           vbest = v;
           ibest = pos;
+          lbest = li;
         }
       }
     }
     {
+      // the perm field carries the local slab row until the CTA candidate is formed
       const int id = warp_argmax_redux(vbest, ibest, ibest >= 0);
-      if (ibest >= 0 && ibest == id) s.wcand[warp] = CCand{vbest, ibest, 0};
+      if (ibest >= 0 && ibest == id) s.wcand[warp] = CCand{vbest, ibest, lbest};
       if (lane == 0 && id < 0) s.wcand[warp] = CCand{0.0, -1, 0};
     }
     CMARK(0);
     __syncthreads();
 
     // ---- (2) CTA candidate -> every CTA of the cluster; publish rows ------------
-    int lc_pub = -1;  // local row of this CTA's candidate (warp 0)
-    if (warp == 0) {
+    int lc_pub = -1;  // local row of this CTA's candidate
+    if (MULTI && spread_pub) {
+      // every warp derives the CTA candidate from the 8 warp candidates (one redux), so
+      // warp 0 sends it while warps 2-5 publish its row and warps 1/6/7 row a, in parallel:
+      // the rows reach L2 before the receivers poll them (one round trip in phase 3)
       const bool ok = lane < kCWarps && s.wcand[lane].idx >= 0;
       const CCand mine = lane < kCWarps ? s.wcand[lane] : CCand{0.0, -1, 0};
       const int id = warp_argmax_redux(mine.v, mine.idx, ok);
@@ -335,43 +373,85 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       CCand c = CCand{0.0, -1, -1};
       if (id >= 0) {
         c = s.wcand[__ffs(bal) - 1];
-        c.perm = s.perm[c.idx - rbase];
-        lc_pub = c.idx - rbase;
-        if (!MULTI) {
-          double* pr = s.pubrow + par * (kmax + 2);
-          for (int j = lane; j <= k; j += 32) pr[j] = s.slab[(size_t)j * Rs + lc_pub];
-        }
+        lc_pub = c.perm;
+        c.perm = s.perm[lc_pub];
       }
-      __syncwarp();
-      if (MULTI) {
-        // candidate -> slot crank of every cluster CTA, delivered with its mbarrier
+      if (warp == 0) {
         if (lane < C) st_async_cand(s.cand + par * kClusterMax + crank, &s.xbar[par], lane, c);
-      } else if (lane < C) {
-        *cluster.map_shared_rank(s.cand + par * kClusterMax + crank, lane) = c;
-      }
-    } else if (!MULTI && warp == 1 && own_a) {
-      const int la = a_pos - rbase;
-      double* pa = s.pubA + par * (kmax + 2);
-      for (int j = lane; j <= k; j += 32) pa[j] = s.slab[(size_t)j * Rs + la];
-      if (lane == 0) s.misc[par] = s.perm[la];
-    }
-    CMARK(1);
-    if (MULTI) {
-      // the global LL publications (candidate row, row a) carry their own flags and
-      // need no ordering; the candidates arrive by st.async on xbar[par] (no
-      // cluster barrier: nothing else is read across CTAs in this mode)
-      if (warp == 0 && lc_pub >= 0) {
-        uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
-        for (int j = lane; j <= k; j += 32) ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc_pub], tag);
-      } else if (warp == 1 && own_a) {
+      } else if (push) {
+        // candidate row [0, k] (pairs of doubles) -> crows[par][crank] of every CTA
+        const int np = (k + 2) >> 1;
+        const int lc = lc_pub >= 0 ? lc_pub : 0;
+        double* dst = s.crows + ((size_t)par * C + crank) * CRS;
+        for (int f = tid - 32; f < C * np; f += kCThreads - 32) {
+          const int d = f / np, pp = f - d * np;
+          const int j0 = 2 * pp;
+          const double x0 = s.slab[(size_t)j0 * Rs + lc];
+          const double x1 = j0 + 1 <= k ? s.slab[(size_t)(j0 + 1) * Rs + lc] : 0.0;
+          st_async_f64x2(dst + j0, &s.xbar[par], uint32_t(d), x0, x1);
+        }
+      } else if (warp >= 2 && warp <= 5) {
+        if (lc_pub >= 0) {
+          uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
+          for (int j = (warp - 2) * 32 + lane; j <= k; j += 128)
+            ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc_pub], tag);
+        }
+      } else if (own_a) {
         const int la = a_pos - rbase;
         uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
-        for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
-        if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
+        const int w3 = warp == 1 ? 0 : warp - 5;
+        for (int j = w3 * 32 + lane; j <= k; j += 96) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
+        if (warp == 1 && lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
       }
+      CMARK(1);
       mbar_wait_acq_cluster(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
     } else {
-      cluster_barrier();
+      if (warp == 0) {
+        const bool ok = lane < kCWarps && s.wcand[lane].idx >= 0;
+        const CCand mine = lane < kCWarps ? s.wcand[lane] : CCand{0.0, -1, 0};
+        const int id = warp_argmax_redux(mine.v, mine.idx, ok);
+        const unsigned bal = __ballot_sync(0xffffffffu, ok && mine.idx == id);
+        CCand c = CCand{0.0, -1, -1};
+        if (id >= 0) {
+          c = s.wcand[__ffs(bal) - 1];
+          lc_pub = c.perm;
+          c.perm = s.perm[lc_pub];
+          if (!MULTI) {
+            double* pr = s.pubrow + par * (kmax + 2);
+            for (int j = lane; j <= k; j += 32) pr[j] = s.slab[(size_t)j * Rs + lc_pub];
+          }
+        }
+        __syncwarp();
+        if (MULTI) {
+          // candidate -> slot crank of every cluster CTA, delivered with its mbarrier
+          if (lane < C) st_async_cand(s.cand + par * kClusterMax + crank, &s.xbar[par], lane, c);
+        } else if (lane < C) {
+          *cluster.map_shared_rank(s.cand + par * kClusterMax + crank, lane) = c;
+        }
+      } else if (!MULTI && warp == 1 && own_a) {
+        const int la = a_pos - rbase;
+        double* pa = s.pubA + par * (kmax + 2);
+        for (int j = lane; j <= k; j += 32) pa[j] = s.slab[(size_t)j * Rs + la];
+        if (lane == 0) s.misc[par] = s.perm[la];
+      }
+      CMARK(1);
+      if (MULTI) {
+        // the global LL publications (candidate row, row a) carry their own flags and
+        // need no ordering; the candidates arrive by st.async on xbar[par] (no
+        // cluster barrier: nothing else is read across CTAs in this mode)
+        if (warp == 0 && lc_pub >= 0) {
+          uint64_t* gr = a.slots + ((size_t)gcta * 2 + par) * a.slot_words + 4;
+          for (int j = lane; j <= k; j += 32) ll_put_double(gr + 2 * j, s.slab[(size_t)j * Rs + lc_pub], tag);
+        } else if (warp == 1 && own_a) {
+          const int la = a_pos - rbase;
+          uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
+          for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
+          if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
+        }
+        mbar_wait_acq_cluster(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
+      } else {
+        cluster_barrier();
+      }
     }
     CMARK(2);
 
@@ -453,14 +533,16 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     const bool swapped = b != a_pos;
     const bool more = (g + 1 < rt) || a.want_y;
     int perm_a = 0;
-    const bool need_a = own_b && swapped;  // row b's owner receives row a
+    const bool need_a = !push && own_b && swapped;  // row b's owner receives row a
     const int lb_thread = (b - rbase) & (kCThreads - 1);
+    if (a.prof) SUBMARK(0);
     // gathers of the next column for every row but b (row b's physical index
     // perm_a arrives with row a; its gather is issued once that is known)
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int li = tid + u * kCThreads;
-      const int pos = rbase + li;
+      int pos = lab[u];  // == rbase + li unless push (then: the label after this step's swap)
+      if (push && swapped) pos = pos == b ? a_pos : (pos == a_pos ? b : pos);
       cnext[u] = 0.0;
       cneg[u] = false;
       if (more && li < rcount && pos > a_pos && !(need_a && pos == b)) {
@@ -470,7 +552,12 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         cnext[u] = cneg[u] ? W[(long long)ph * ld + pb] : W[(long long)pb * ld + ph];
       }
     }
-    if (MULTI) {
+    if (a.prof) SUBMARK(1);
+    if (push) {
+      // the winner's row arrived with its candidate
+      const double* cr = s.crows + ((size_t)par * C + owner) * CRS;
+      for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = cr[j];
+    } else if (MULTI) {
       const uint64_t* gr = a.pivot ? a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4
                                    : a.rowa + (size_t)par * a.slot_words + 4;
       const uint64_t* ra = a.rowa + (size_t)par * a.slot_words;
@@ -500,6 +587,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = wr[j];
       }
     }
+    if (a.prof) SUBMARK(2);
     if (need_a && tid == lb_thread) {
       const int u = (b - rbase) >> 8;  // kCThreads == 256
 #pragma unroll
@@ -513,7 +601,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     CMARK(3);
 
     // ---- (4) interchange rows a/b, scale column k, z for the next step -------
-    if (swapped) {
+    if (swapped && !push) {
       if (own_a) {
         const int la = a_pos - rbase;
         for (int j = tid; j < k; j += kCThreads) s.slab[(size_t)j * Rs + la] = s.wrow[j];
@@ -542,7 +630,20 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int li = tid + u * kCThreads;
-      if (li < rcount) {
+      if (li < rcount && push) {
+        // lazy interchange: labels a <-> b swap, the rows' data stay
+        int pos = lab[u];
+        if (swapped) {
+          pos = pos == b ? a_pos : (pos == a_pos ? b : pos);
+          lab[u] = pos;
+        }
+        if (pos == a_pos) {
+          col[li] = 1.0;
+        } else if (pos > a_pos) {
+          const double v = col[li];
+          col[li] = vb != 0.0 ? v / vb : v;
+        }
+      } else if (li < rcount) {
         const int pos = rbase + li;
         if (pos == a_pos) {
           col[li] = 1.0;
@@ -587,7 +688,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int li = tid + u * kCThreads;
-        if (li < rcount && rbase + li > a_pos) {
+        if (li < rcount && lab[u] > a_pos) {
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
           int j = 0;
           if (u == 0 && nbank > 0) {
@@ -634,28 +735,30 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   }
   if (a.prof && tid == 0) {
     for (int i = 0; i < 6; ++i) a.prof[cta * 16 + i] += (unsigned long long)pt[i];
+    for (int i = 0; i < 3; ++i) a.prof[cta * 16 + 12 + i] += (unsigned long long)sub[i];
     a.prof[cta * 16 + 6] += (unsigned long long)(rt - r);
     a.prof[cta * 16 + 8] += (unsigned long long)(t_loop0 - t_kernel0);
     a.prof[cta * 16 + 9] += (unsigned long long)(clock64() - t_prev);
   }
-  if (a.want_y) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int li = tid + u * kCThreads;
-      if (li < rcount) s.ycol[li] = cneg[u] ? -cnext[u] : cnext[u];
+  for (int u = 0; u < 2; ++u) {
+    const int li = tid + u * kCThreads;
+    if (li < rcount) {
+      s.lab[li] = lab[u];
+      if (a.want_y) s.ycol[li] = cneg[u] ? -cnext[u] : cnext[u];
     }
   }
   __syncthreads();
 
   // ---- var1: y = column rt after the couplings (straggler operand) --------
   if (a.want_y && rt < n) {
-    const int l0 = max(0, rt + 1 - rbase);
-    for (int li = l0 + tid; li < rcount; li += kCThreads) a.y[rbase + li] = s.ycol[li] - s.az[li];
+    for (int li = tid; li < rcount; li += kCThreads)
+      if (s.lab[li] >= rt + 1) a.y[s.lab[li]] = s.ycol[li] - s.az[li];
   }
 
   // ---- materialise displaced trailing lines, write back ------------------
   for (int li = tid; li < rcount; li += kCThreads) {
-    int pos = rbase + li, ph = s.perm[li];
+    int pos = s.lab[li], ph = s.perm[li];
     a.gperm[pos] = ph;
     if (pos >= rt && ph != pos) {
       int q = atomicAdd(a.disp_count, 1);
@@ -672,7 +775,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     // columns with every SM instead of this kernel's 16: the displaced lines are
     // row accesses of column-major storage (one sector per element)
     for (int li = tid; li < rcount; li += kCThreads) {
-      double* dst = a.pbuf + rbase + li;
+      double* dst = a.pbuf + s.lab[li];
       int j = 0;
       for (; j + 8 <= kmax; j += 8) {  // 8 loads in flight, then 8 streaming stores
         double v[8];
@@ -746,7 +849,9 @@ cudaError_t launch_panel_finish(const PanelArgs& a, cudaStream_t stream) {
 
 }  // namespace
 
-size_t panel_cluster_smem_bytes(int rows_per, int kmax) { return csmem_layout(rows_per, kmax, nullptr, nullptr); }
+size_t panel_cluster_smem_bytes(int rows_per, int kmax, int npush) {
+  return csmem_layout(rows_per, kmax, nullptr, nullptr, npush);
+}
 
 int panel_cluster_size() {
   static int cs = -1;
@@ -832,7 +937,8 @@ int panel_multi_clusters(int csize, size_t smem) {
 
 // a.nblocks = total CTAs (Q clusters x a.csize); cooperative so all clusters are co-resident
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream) {
-  size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr);
+  const bool push = a.push && a.pivot && a.nblocks == csize;
+  size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr, push ? csize : 0);
   cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

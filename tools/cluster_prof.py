@@ -23,4 +23,5 @@ for c in ([0, 7, 15] if n <= 8192 else [0, 8, 63, 127]):
     tot = p[c, :6].sum()
     print(f"cta {c}: {tot/steps:.0f} cyc/step over {steps} steps: " + ", ".join(f"{names[i]}={p[c,i]/steps:.0f}" for i in range(6))
           + (f"; kernel total {p[c,7]/1e6:.2f} Mcyc, outside the step loop {(p[c,7]-tot)/1e6:.2f} Mcyc"
-             f" (prologue {p[c,8]/1e6:.2f}, loop-end..prof {p[c,9]/1e6:.2f}, start..gperm {p[c,10]/1e6:.2f}, pbuf {p[c,11]/1e6:.2f})" if p[c, 7] else ""))
+             f" (prologue {p[c,8]/1e6:.2f}, loop-end..prof {p[c,9]/1e6:.2f}, start..gperm {p[c,10]/1e6:.2f}, pbuf {p[c,11]/1e6:.2f})" if p[c, 7] else "")
+          + f"; phase 3 cumulative: winner {p[c,12]/steps:.0f}, gathers issued {p[c,13]/steps:.0f}, row poll {p[c,14]/steps:.0f}")
