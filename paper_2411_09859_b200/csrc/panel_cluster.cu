@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   long long sub[3] = {0, 0, 0};  // phase-3 split (profiling only): winner | gathers issued | row poll done
   long long t_prev = clock64();
   const long long t_loop0 = t_prev;
+#ifdef SKL_PANEL_PROFILE
 #define SUBMARK(i)                  \
   do {                              \
     sub[i] += clock64() - t_prev;   \
@@ -302,6 +303,14 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     pt[i] += _t - t_prev;           \
     t_prev = _t;                    \
   } while (0)
+#else  // phase clocks only in the profiling build (make prof)
+#define SUBMARK(i) \
+  do {             \
+  } while (0)
+#define CMARK(i) \
+  do {           \
+  } while (0)
+#endif
 
   // register cache of slab columns [0, kBank*nbank) for row li = tid (the gemv re-reads
   // the slab every step; shared-memory bandwidth is its bound otherwise)
@@ -383,8 +392,9 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         const int np = (k + 2) >> 1;
         const int lc = lc_pub >= 0 ? lc_pub : 0;
         double* dst = s.crows + ((size_t)par * C + crank) * CRS;
+        const float inv_np = 1.0f / float(np);  // f < 16 * 66: the float quotient is exact after rz
         for (int f = tid - 32; f < C * np; f += kCThreads - 32) {
-          const int d = f / np, pp = f - d * np;
+          const int d = __float2int_rz((float(f) + 0.5f) * inv_np), pp = f - d * np;
           const int j0 = 2 * pp;
           const double x0 = s.slab[(size_t)j0 * Rs + lc];
           const double x1 = j0 + 1 <= k ? s.slab[(size_t)(j0 + 1) * Rs + lc] : 0.0;
@@ -458,6 +468,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     // ---- (3) winner, next-column gather, winner row / row a via DSMEM ---------
     int owner;
     CCand w;
+    const double* xrow = s.wrow;  // pivot row of this step (push: in place in crows)
     {
       const bool ok = lane < C && s.cand[par * kClusterMax + lane].idx >= 0;
       const CCand mine = lane < C ? s.cand[par * kClusterMax + lane] : CCand{0.0, -1, -1};
@@ -535,7 +546,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     int perm_a = 0;
     const bool need_a = !push && own_b && swapped;  // row b's owner receives row a
     const int lb_thread = (b - rbase) & (kCThreads - 1);
-    if (a.prof) SUBMARK(0);
+    SUBMARK(0);
     // gathers of the next column for every row but b (row b's physical index
     // perm_a arrives with row a; its gather is issued once that is known)
 #pragma unroll
@@ -552,11 +563,10 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         cnext[u] = cneg[u] ? W[(long long)ph * ld + pb] : W[(long long)pb * ld + ph];
       }
     }
-    if (a.prof) SUBMARK(1);
+    SUBMARK(1);
     if (push) {
-      // the winner's row arrived with its candidate
-      const double* cr = s.crows + ((size_t)par * C + owner) * CRS;
-      for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = cr[j];
+      // the winner's row arrived with its candidate: phase 4 reads it in place
+      xrow = s.crows + ((size_t)par * C + owner) * CRS;
     } else if (MULTI) {
       const uint64_t* gr = a.pivot ? a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4
                                    : a.rowa + (size_t)par * a.slot_words + 4;
@@ -587,7 +597,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         for (int j = tid; j <= k; j += kCThreads) s.wrow[j] = wr[j];
       }
     }
-    if (a.prof) SUBMARK(2);
+    SUBMARK(2);
     if (need_a && tid == lb_thread) {
       const int u = (b - rbase) >> 8;  // kCThreads == 256
 #pragma unroll
@@ -597,7 +607,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
           cnext[uu] = cneg[uu] ? W[(long long)perm_a * ld + pb] : W[(long long)pb * ld + perm_a];
         }
     }
-    __syncthreads();
+    if (!push) __syncthreads();  // push: nothing phase 4 reads was written by another thread here
     CMARK(3);
 
     // ---- (4) interchange rows a/b, scale column k, z for the next step -------
@@ -657,8 +667,8 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       }
     }
     for (int j = tid; j <= k; j += kCThreads) {
-      const double xm = j >= 1 ? s.wrow[j - 1] : 0.0;
-      const double xp = (j + 1 < k) ? s.wrow[j + 1] : (j + 1 == k ? 1.0 : 0.0);
+      const double xm = j >= 1 ? xrow[j - 1] : 0.0;
+      const double xp = (j + 1 < k) ? xrow[j + 1] : (j + 1 == k ? 1.0 : 0.0);
       const double tj = j == k ? vb : s.taus[j];
       const double tj1 = (j + 1 == k) ? vb : s.taus[j + 1];
       s.zbuf[j] = (j >= 1 ? tj * xm : 0.0) - (j + 1 <= k ? tj1 * xp : 0.0);
@@ -689,38 +699,64 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
       for (int u = 0; u < 2; ++u) {
         const int li = tid + u * kCThreads;
         if (li < rcount && lab[u] > a_pos) {
-          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          // eight independent FMA chains (the phase is bound by the chain latency)
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, a5 = 0.0, a6 = 0.0, a7 = 0.0;
           int j = 0;
           if (u == 0 && nbank > 0) {
             const double2* z2 = reinterpret_cast<const double2*>(s.zbuf);
 #pragma unroll
-            for (int q = 0; q < kBank; q += 4) {
-              const double2 za = z2[q >> 1], zb = z2[(q >> 1) + 1];
+            for (int q = 0; q < kBank; q += 8) {
+              const double2 za = z2[q >> 1], zb = z2[(q >> 1) + 1], zc = z2[(q >> 1) + 2], zd = z2[(q >> 1) + 3];
               a0 = fma(rb[0][q], za.x, a0);
               a1 = fma(rb[0][q + 1], za.y, a1);
               a2 = fma(rb[0][q + 2], zb.x, a2);
               a3 = fma(rb[0][q + 3], zb.y, a3);
+              a4 = fma(rb[0][q + 4], zc.x, a4);
+              a5 = fma(rb[0][q + 5], zc.y, a5);
+              a6 = fma(rb[0][q + 6], zd.x, a6);
+              a7 = fma(rb[0][q + 7], zd.y, a7);
             }
             if (nbank > 1) {
 #pragma unroll
-              for (int q = 0; q < kBank; q += 4) {
-                const double2 za = z2[(kBank + q) >> 1], zb = z2[((kBank + q) >> 1) + 1];
+              for (int q = 0; q < kBank; q += 8) {
+                const int h = (kBank + q) >> 1;
+                const double2 za = z2[h], zb = z2[h + 1], zc = z2[h + 2], zd = z2[h + 3];
                 a0 = fma(rb[1][q], za.x, a0);
                 a1 = fma(rb[1][q + 1], za.y, a1);
                 a2 = fma(rb[1][q + 2], zb.x, a2);
                 a3 = fma(rb[1][q + 3], zb.y, a3);
+                a4 = fma(rb[1][q + 4], zc.x, a4);
+                a5 = fma(rb[1][q + 5], zc.y, a5);
+                a6 = fma(rb[1][q + 6], zd.x, a6);
+                a7 = fma(rb[1][q + 7], zd.y, a7);
               }
             }
             j = kBank * nbank;
           }
-          for (; j + 3 < kk; j += 4) {
+          for (; j + 7 < kk; j += 8) {
             a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
             a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
             a2 = fma(s.slab[(size_t)(j + 2) * Rs + li], s.zbuf[j + 2], a2);
             a3 = fma(s.slab[(size_t)(j + 3) * Rs + li], s.zbuf[j + 3], a3);
+            a4 = fma(s.slab[(size_t)(j + 4) * Rs + li], s.zbuf[j + 4], a4);
+            a5 = fma(s.slab[(size_t)(j + 5) * Rs + li], s.zbuf[j + 5], a5);
+            a6 = fma(s.slab[(size_t)(j + 6) * Rs + li], s.zbuf[j + 6], a6);
+            a7 = fma(s.slab[(size_t)(j + 7) * Rs + li], s.zbuf[j + 7], a7);
           }
-          for (; j < kk; ++j) a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
-          s.az[li] = kk >= 2 ? (a0 + a1) + (a2 + a3) : 0.0;
+          if (j + 3 < kk) {
+            a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
+            a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
+            a2 = fma(s.slab[(size_t)(j + 2) * Rs + li], s.zbuf[j + 2], a2);
+            a3 = fma(s.slab[(size_t)(j + 3) * Rs + li], s.zbuf[j + 3], a3);
+            j += 4;
+          }
+          if (j + 1 < kk) {
+            a4 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a4);
+            a5 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a5);
+            j += 2;
+          }
+          if (j < kk) a6 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a6);
+          s.az[li] = kk >= 2 ? ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7)) : 0.0;
         }
       }
     }
