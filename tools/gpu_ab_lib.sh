@@ -12,4 +12,7 @@ done; done
 for L in $OLD $NEW; do
   echo "$(basename $L) $(SKEWLTL_B200_LIB=$L timeout 300 python tools/kernel_split.py 16384 256 2>&1 | tail -1)" >> gpurun_out/ab.log
 done
-SKEWLTL_B200_LIB=paper_2411_09859_b200/_lib/libskewltl_b200_prof.so timeout 200 python tools/cluster_prof.py 4096 128 > gpurun_out/ab_prof.log 2>&1
+for L in $OLD $NEW; do
+  echo "$(basename $L) $(SKEWLTL_B200_LIB=$L timeout 300 python tools/time_batched.py 2>&1 | tail -2 | tr '\n' ' ')" >> gpurun_out/ab.log
+done
+timeout 600 python -m pytest tests/test_gpu_batched.py -x -q -m gpu > gpurun_out/ab_tests_b.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tests_b.log
