@@ -184,51 +184,6 @@ __host__ __device__ inline size_t csmem_layout(int R, int kmax, CSmem* s, unsign
   return off;
 }
 
-// az[li] = sum_{j<k} slab[j][li] z_j for local rows li >= l0 (G groups split k)
-__device__ __forceinline__ void compute_az(const CSmem& s, int Rs, int R, int rcount, int G, int k, int l0,
-                                           int tid) {
-  if (k < 2) {
-    for (int li = tid; li < rcount; li += kCThreads) s.az[li] = 0.0;
-    return;
-  }
-  if (G > 1) {
-    if (tid < G * R) {
-      const int gi = tid / R, li = tid - gi * R;
-      if (li >= l0 && li < rcount) {
-        const int kc = (k + G - 1) / G;
-        const int j0 = gi * kc, j1 = min(k, j0 + kc);
-        double a0 = 0.0, a1 = 0.0;
-        int j = j0;
-        for (; j + 1 < j1; j += 2) {
-          a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
-          a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
-        }
-        if (j < j1) a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
-        s.part[gi * R + li] = a0 + a1;
-      }
-    }
-    __syncthreads();
-    for (int li = l0 + tid; li < rcount; li += kCThreads) {
-      double acc = 0.0;
-      for (int gi = 0; gi < G; ++gi) acc += s.part[gi * R + li];
-      s.az[li] = acc;
-    }
-  } else {
-    for (int li = l0 + tid; li < rcount; li += kCThreads) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int j = 0;
-      for (; j + 3 < k; j += 4) {
-        a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
-        a1 = fma(s.slab[(size_t)(j + 1) * Rs + li], s.zbuf[j + 1], a1);
-        a2 = fma(s.slab[(size_t)(j + 2) * Rs + li], s.zbuf[j + 2], a2);
-        a3 = fma(s.slab[(size_t)(j + 3) * Rs + li], s.zbuf[j + 3], a3);
-      }
-      for (; j < k; ++j) a0 = fma(s.slab[(size_t)j * Rs + li], s.zbuf[j], a0);
-      s.az[li] = (a0 + a1) + (a2 + a3);
-    }
-  }
-}
-
 // MULTI = several co-resident clusters (cooperative launch): candidates are
 // reduced inside each cluster through DSMEM, then the cluster leaders exchange
 // their cluster's best through global LL records; pivot rows travel through L2.
@@ -246,7 +201,6 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n, lo = a.lo, r = a.r, nelim = a.nelim, kmax = a.kmax;
   const int R = a.rows_per, Rs = cslab_stride(R);
-  const int G = R <= kCThreads ? max(1, min(kCThreads / max(R, 1), 16)) : 1;
   const long long ld = a.ld;
   double* __restrict__ W = a.W;
   const int row0 = lo + 1;
