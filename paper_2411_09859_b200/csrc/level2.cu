@@ -176,8 +176,13 @@ cudaError_t launch_skew_tridiag_gemv(double* y, double alpha, const double* A, l
   if (rows <= 0) return cudaSuccess;
   int grid = (rows + 255) / 256;
   if (grid > 1184) grid = 1184;
-  skew_tridiag_gemv_kernel<<<grid, 256, sizeof(double) * (k > 0 ? k : 1), stream>>>(y, alpha, A, lda, p, k, tau, x,
-                                                                                    beta, tail_from);
+  const size_t zbytes = sizeof(double) * (k > 0 ? k : 1);  // z = T x staged in shared memory
+  if (zbytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(skew_tridiag_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)zbytes);
+    if (e != cudaSuccess) return e;  // k beyond the shared-memory budget (~29K columns)
+  }
+  skew_tridiag_gemv_kernel<<<grid, 256, zbytes, stream>>>(y, alpha, A, lda, p, k, tau, x, beta, tail_from);
   return cudaGetLastError();
 }
 

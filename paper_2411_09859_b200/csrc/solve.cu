@@ -26,28 +26,35 @@ __device__ __forceinline__ double l_at(const double* __restrict__ L, long long l
 }
 
 // perm[i] with (P x)[i] = x[perm[i]] (core.py:274-285): the swap chain runs in
-// shared memory (one thread), the result is written out coalesced
-__global__ void compose_perm_kernel(int n, const long long* __restrict__ piv, int* __restrict__ perm) {
-  extern __shared__ int sp[];
-  int* soff = sp + n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    sp[i] = i;
-    soff[i] = int(piv[i]);
-  }
+// shared memory (one thread; n ints of dynamic shared memory, or perm itself in
+// global memory when n does not fit), the offsets are staged in chunks and the
+// result is written out coalesced
+constexpr int kPermChunk = 2048;
+__global__ void compose_perm_kernel(int n, const long long* __restrict__ piv, int* __restrict__ perm, int in_smem) {
+  extern __shared__ int sp_dyn[];
+  __shared__ int soff[kPermChunk];
+  int* sp = in_smem ? sp_dyn : perm;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sp[i] = i;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < n; ++k) {
-      const int off = soff[k];
-      if (off) {
-        const int j = k + int(off);
-        const int t = sp[k];
-        sp[k] = sp[j];
-        sp[j] = t;
+  for (int k0 = 0; k0 < n; k0 += kPermChunk) {
+    const int k1 = min(n, k0 + kPermChunk);
+    for (int t = threadIdx.x; t < k1 - k0; t += blockDim.x) soff[t] = int(piv[k0 + t]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = k0; k < k1; ++k) {
+        const int off = soff[k - k0];
+        if (off) {
+          const int j = k + off;
+          const int t = sp[k];
+          sp[k] = sp[j];
+          sp[j] = t;
+        }
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = sp[i];
+  if (in_smem)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = sp[i];
 }
 
 // dst = src[perm] (gather) or dst[perm] = src (scatter), column-major n x nrhs
@@ -346,10 +353,42 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
   const long long ldz = n;
   cudaError_t err = cudaMemsetAsync(info, 0, sizeof(int), stream);
   if (err != cudaSuccess) return err;
-  compose_perm_kernel<<<1, 256, 2 * sizeof(int) * n, stream>>>(n, piv, perm);
+  {
+    // the swap chain in shared memory when n ints fit next to the static chunk buffer
+    static int optin = 0;
+    if (optin == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
+        optin = 48 * 1024;
+      optin -= int(sizeof(int)) * kPermChunk + 1024;
+    }
+    const size_t pbytes = sizeof(int) * (size_t)n;
+    const int in_smem = pbytes <= (size_t)optin ? 1 : 0;
+    if (in_smem && pbytes > 48 * 1024) {
+      err = cudaFuncSetAttribute(compose_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pbytes);
+      if (err != cudaSuccess) return err;
+    }
+    compose_perm_kernel<<<1, 256, in_smem ? pbytes : 0, stream>>>(n, piv, perm, in_smem);
+  }
   const long long tot = (long long)n * nrhs;
   const int pg = int(std::min<long long>((tot + 255) / 256, 148 * 8));
   permute_rows_kernel<<<pg, 256, 0, stream>>>(n, nrhs, B, ldb, Z, ldz, perm, 0);
+  // the tridiagonal factorization depends on tau only: it runs on a side stream,
+  // overlapped with the permutation and the forward sweep (one thread's sequential
+  // recurrence, ~0.6 ms at n = 4096, would otherwise sit on the critical path)
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (side == nullptr) {
+    if ((err = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) != cudaSuccess) return err;
+    if ((err = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming)) != cudaSuccess) return err;
+    if ((err = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming)) != cudaSuccess) return err;
+  }
+  if ((err = cudaEventRecord(ev_fork, stream)) != cudaSuccess) return err;  // info zeroed, inputs ready
+  if ((err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return err;
+  tridiag_factor_kernel<<<1, 256, 0, side>>>(n, tau, tol_scale, d, e, f2, mult, swp, info);
+  tridiag_recip_kernel<<<(n + 255) / 256, 256, 0, side>>>(n, d, info);
+  if ((err = cudaEventRecord(ev_join, side)) != cudaSuccess) return err;
   // L z = P b (forward, blocks of 64 columns)
   for (int j0 = 0; j0 < n; j0 += kSolveBlk) {
     const int j1 = std::min(n, j0 + kSolveBlk);
@@ -360,8 +399,7 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
       trsm_update_down_kernel<<<grid, 64, 0, stream>>>(n, nrhs, L, ldl, Z, ldz, j0, j1);
     }
   }
-  tridiag_factor_kernel<<<1, 256, 0, stream>>>(n, tau, tol_scale, d, e, f2, mult, swp, info);
-  tridiag_recip_kernel<<<(n + 255) / 256, 256, 0, stream>>>(n, d, info);
+  if ((err = cudaStreamWaitEvent(stream, ev_join, 0)) != cudaSuccess) return err;
   tridiag_apply_kernel<<<nrhs, 128, 0, stream>>>(n, nrhs, d, e, f2, mult, swp, info, Z, ldz);
   // L^T y = z (backward)
   const int nblk = (n + kSolveBlk - 1) / kSolveBlk;

@@ -60,3 +60,20 @@ def test_solve_singular_odd(n):
 def test_solve_dimension_mismatch():
     with pytest.raises(ValueError):
         pk().solve(pk().SkewMatrixLower(skew_lower(8, 0)), np.ones(7))
+
+
+@pytest.mark.parametrize("n,nrhs", [(8192, 1), (8192, 6), (16384, 2)])
+def test_solve_large_n_residual(n, nrhs):
+    """Sizes past the 48 KB default shared-memory window of the permutation
+    composition (n > 6144): device-resident X and b, residual on the device."""
+    import torch
+    from paper_2411_09859_b200 import device as dv
+    x = skew_lower(n, 3)
+    xd = dv.to_device_colmajor(x)
+    b = torch.randn(n, nrhs, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(n))
+    y = pk().solve(pk().SkewMatrixLower(xd), b)
+    Xd = torch.tril(xd, -1)
+    Xd = Xd - Xd.T
+    r = Xd @ y - b
+    eps = np.finfo(float).eps
+    assert float(torch.linalg.norm(r)) <= 10 * eps * n * float(torch.linalg.norm(Xd)) * float(torch.linalg.norm(y))
