@@ -171,6 +171,24 @@ def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush):
         ltlt_unb_twostep_device(x1, True)
     ms = _time(torch, lambda: ltlt_unb_twostep_device(x1, True), 10, e0, e1)
     res["config1_twostep_n512"] = {"ms": round(ms, 4), "gflops": round(512 ** 3 / 3 / (ms * 1e-3) / 1e9, 2)}
+    # solve X y = b after the config-2 factorization (device-resident factors)
+    from paper_2411_09859_b200 import _capi
+    x2 = dv.to_device_colmajor(skew_lower(4096, 0))
+    L2, t2, p2 = pk.ltlt_blk_piv_device(x2, 128, "var1")
+    lib = _capi.load()
+    for nrhs in (1, 128):
+        B = torch.randn(4096, nrhs, dtype=torch.float64, device="cuda").t().contiguous().t()
+        nbw = lib.skl_ltlt_solve_workspace_size(4096, nrhs)
+        ws = dv.workspace(nbw)
+        info = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+        def one(B=B, nrhs=nrhs, ws=ws, nbw=nbw, info=info):
+            lib.skl_ltlt_solve(4096, nrhs, L2.data_ptr(), 4096, t2.data_ptr(), p2.data_ptr(), B.data_ptr(), 4096,
+                               10.0, info.data_ptr(), ws.data_ptr(), nbw, dv.stream_ptr())
+        one()
+        ms = _time(torch, one, 5, e0, e1)
+        res[f"solve_n4096_nrhs{nrhs}"] = {"ms": round(ms, 3)}
+    del x2, L2
     # config 3: blocked n=16384, nb=256, U(-1,1)
     x3 = dv.to_device_colmajor(skew_lower(16384, 0, "uniform"))
     L3 = dv.empty_colmajor(16384, 16384, torch.float64)
