@@ -158,6 +158,83 @@ __global__ void trsm_update_up_kernel(int n, int nrhs, const double* __restrict_
   }
 }
 
+// One launch per 64-column block (instead of a diagonal launch + an update launch):
+// every CTA stages and solves the diagonal block of its right-hand side itself (the
+// same arithmetic as trsm_diag_kernel, so all CTAs hold the same solution), CTA 0
+// writes the solved block to the OTHER buffer (zout: nobody in this launch reads it),
+// and the CTA updates its share of the remaining rows of zin from shared memory (as
+// trsm_update_*).  Forward: Z -> B (B is free scratch between the gather and the final
+// scatter); backward: B -> Z.  Bit-identical to the two-launch scheme.
+template <bool TRANS>
+__global__ void __launch_bounds__(256) trsm_fused_kernel(int n, const double* __restrict__ L, long long ld,
+                                                         double* __restrict__ zin_all, long long ldi,
+                                                         double* __restrict__ zout_all, long long ldo, int j0,
+                                                         int j1) {
+  __shared__ double lb[kSolveBlk][kSolveBlk + 1];  // lb[col][row] = L[j0+row, j0+col]
+  __shared__ double zb[kSolveBlk];
+  const int c = blockIdx.y;
+  double* zin = zin_all + (long long)c * ldi;
+  double* zout = zout_all + (long long)c * ldo;
+  const int w = j1 - j0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int cc = warp; cc < w; cc += nw) {
+    const double* col = j0 + cc >= 1 ? L + (long long)(j0 + cc - 1) * ld + j0 : nullptr;
+    const double v0 = (col && lane > cc && lane < w) ? col[lane] : 0.0;
+    const double v1 = (col && lane + 32 > cc && lane + 32 < w) ? col[lane + 32] : 0.0;
+    lb[cc][lane] = v0;
+    lb[cc][lane + 32] = v1;
+  }
+  for (int t = threadIdx.x; t < w; t += blockDim.x) zb[t] = zin[j0 + t];
+  __syncthreads();
+  if (!TRANS) {
+    for (int jj = 0; jj < w; ++jj) {
+      const double y = zb[jj];
+      for (int t = jj + 1 + threadIdx.x; t < w; t += blockDim.x) zb[t] -= lb[jj][t] * y;
+      __syncthreads();
+    }
+  } else {
+    for (int jj = w - 1; jj >= 0; --jj) {
+      const double y = zb[jj];
+      for (int t = threadIdx.x; t < jj; t += blockDim.x) zb[t] -= lb[t][jj] * y;
+      __syncthreads();
+    }
+  }
+  if (blockIdx.x == 0)
+    for (int t = threadIdx.x; t < w; t += blockDim.x) zout[j0 + t] = zb[t];
+  if (!TRANS) {
+    // rows below the block, thread per row
+    for (int i = j1 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int t = 0;
+      if (w == kSolveBlk) {
+#pragma unroll 16
+        for (; t < kSolveBlk; t += 4) {
+          a0 = fma(l_at(L, ld, i, j0 + t), zb[t], a0);
+          a1 = fma(l_at(L, ld, i, j0 + t + 1), zb[t + 1], a1);
+          a2 = fma(l_at(L, ld, i, j0 + t + 2), zb[t + 2], a2);
+          a3 = fma(l_at(L, ld, i, j0 + t + 3), zb[t + 3], a3);
+        }
+      }
+      for (; t < w; ++t) a0 = fma(l_at(L, ld, i, j0 + t), zb[t], a0);
+      zin[i] -= (a0 + a1) + (a2 + a3);
+    }
+  } else {
+    // rows above the block, warp per row
+    for (int i = blockIdx.x * nw + warp; i < j0; i += gridDim.x * nw) {
+      double acc = 0.0;
+      if (i >= 1) {
+        const double* col = L + (long long)(i - 1) * ld + j0;
+        const double v0 = lane < w ? col[lane] : 0.0;
+        const double v1 = lane + 32 < w ? col[lane + 32] : 0.0;
+        acc = fma(v0, lane < w ? zb[lane] : 0.0, v1 * (lane + 32 < w ? zb[lane + 32] : 0.0));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) zin[i] -= acc;
+    }
+  }
+}
+
 constexpr int kChunk = 512;  // steps staged in shared memory per round
 
 // factor T (subdiagonal tau) by Gaussian elimination with partial pivoting, one
@@ -389,22 +466,41 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
   tridiag_factor_kernel<<<1, 256, 0, side>>>(n, tau, tol_scale, d, e, f2, mult, swp, info);
   tridiag_recip_kernel<<<(n + 255) / 256, 256, 0, side>>>(n, d, info);
   if ((err = cudaEventRecord(ev_join, side)) != cudaSuccess) return err;
-  // L z = P b (forward, blocks of 64 columns)
+  // fused launches for one or two right-hand sides (n=4096, 1 rhs: 2.52 -> 2.24 ms); with
+  // many the redundant per-CTA diagonal solves and L reads lose (16 rhs: 3.0 -> 5.1 ms)
+  static const bool fused_on = [] {
+    const char* v = getenv("SKL_SOLVE_FUSED");
+    return !(v && *v == '0');
+  }();
+  const bool fused = fused_on && nrhs <= 2;
+  // L z = P b (forward, blocks of 64 columns); fused: the solved z lands in B
   for (int j0 = 0; j0 < n; j0 += kSolveBlk) {
     const int j1 = std::min(n, j0 + kSolveBlk);
+    const int rows = n - j1;
+    if (fused) {
+      dim3 grid(std::max(1, std::min((rows + 255) / 256, 148 * 2)), nrhs);
+      trsm_fused_kernel<false><<<grid, 256, 0, stream>>>(n, L, ldl, Z, ldz, B, ldb, j0, j1);
+      continue;
+    }
     trsm_diag_kernel<false><<<nrhs, 256, 0, stream>>>(n, L, ldl, Z, ldz, j0, j1);
     if (j1 < n) {
-      const int rows = n - j1;
       dim3 grid(std::max(1, std::min((rows + 63) / 64, 148 * 8)), nrhs);
       trsm_update_down_kernel<<<grid, 64, 0, stream>>>(n, nrhs, L, ldl, Z, ldz, j0, j1);
     }
   }
+  double* Zt = fused ? B : Z;  // the forward solution
+  const long long ldt = fused ? ldb : ldz;
   if ((err = cudaStreamWaitEvent(stream, ev_join, 0)) != cudaSuccess) return err;
-  tridiag_apply_kernel<<<nrhs, 128, 0, stream>>>(n, nrhs, d, e, f2, mult, swp, info, Z, ldz);
-  // L^T y = z (backward)
+  tridiag_apply_kernel<<<nrhs, 128, 0, stream>>>(n, nrhs, d, e, f2, mult, swp, info, Zt, ldt);
+  // L^T y = z (backward); fused: the solved y lands back in Z
   const int nblk = (n + kSolveBlk - 1) / kSolveBlk;
   for (int bi = nblk - 1; bi >= 0; --bi) {
     const int j0 = bi * kSolveBlk, j1 = std::min(n, j0 + kSolveBlk);
+    if (fused) {
+      dim3 grid(std::max(1, std::min((j0 + 7) / 8, 148 * 4)), nrhs);
+      trsm_fused_kernel<true><<<grid, 256, 0, stream>>>(n, L, ldl, B, ldb, Z, ldz, j0, j1);
+      continue;
+    }
     trsm_diag_kernel<true><<<nrhs, 256, 0, stream>>>(n, L, ldl, Z, ldz, j0, j1);
     if (j0 > 0) {
       dim3 grid(std::max(1, std::min((j0 + 7) / 8, 148 * 4)), nrhs);
