@@ -139,9 +139,8 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
     if (C < 2) C = 2;
     if (C > Cmax) C = Cmax;
     int Rc = (rows + C - 1) / C;
-    // the cluster kernels hold at most two rows per thread (R <= 512).  Known issue: a
-    // plan whose single-cluster panels reach R ~ 512 after multi-cluster panels (only via
-    // SKL_MIN_CLUSTER_W < 56 with n > 8192) faults; the default floor (64) never builds one
+    // the cluster kernels hold at most two rows per thread (R <= 512); a larger R
+    // (reachable with SKL_MIN_CLUSTER_W < 56) used to fault
     if (Rc <= 2 * skl::panel_threads()) {
       static int min_w = env_int("SKL_MIN_CLUSTER_W", 64);
       static int ll_single = env_int("SKL_LL_SINGLE", 1);
