@@ -292,8 +292,10 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
 
     if (MULTI && tid == 0) {
       // this step's deliveries: C candidates (16 B each) and the global winner (16 B)
-      const uint32_t rowb = push ? 16u * uint32_t((k + 2) >> 1) : 0u;
-      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C) * (uint32_t(sizeof(CCand)) + rowb));
+      // push mode: the candidate rows complete on their own barrier (xbar[2 + par], unused
+      // with one cluster), so the winner is found while the rows are still in flight
+      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C) * uint32_t(sizeof(CCand)));
+      if (push) mbar_arrive_expect_tx(&s.xbar[2 + par], uint32_t(C) * 16u * uint32_t((k + 2) >> 1));
       if (Q > 1) mbar_arrive_expect_tx(&s.xbar[2 + par], sizeof(CCand));
     }
 
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
           const int j0 = 2 * pp;
           const double x0 = s.slab[(size_t)j0 * Rs + lc];
           const double x1 = j0 + 1 <= k ? s.slab[(size_t)(j0 + 1) * Rs + lc] : 0.0;
-          st_async_f64x2(dst + j0, &s.xbar[par], uint32_t(d), x0, x1);
+          st_async_f64x2(dst + j0, &s.xbar[2 + par], uint32_t(d), x0, x1);
         }
       } else if (warp >= 2 && warp <= 5) {
         if (lc_pub >= 0) {
@@ -519,7 +521,8 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     }
     SUBMARK(1);
     if (push) {
-      // the winner's row arrived with its candidate: phase 4 reads it in place
+      // the winner's row (pushed with its candidate) is read in place by phase 4
+      mbar_wait_acq_cluster(&s.xbar[2 + par], (uint32_t(g - r) >> 1) & 1u);
       xrow = s.crows + ((size_t)par * C + owner) * CRS;
     } else if (MULTI) {
       const uint64_t* gr = a.pivot ? a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4
