@@ -366,7 +366,7 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def panel_dram_traffic(path=Path(__file__).resolve().parent / "profiles" / "r01_panel_dram_n4096_v7.csv"):
+def panel_dram_traffic(path=Path(__file__).resolve().parent / "profiles" / "r01_panel_dram_n4096_v10.csv"):
     """Mean DRAM bytes (read + write) per panel_cluster_kernel launch of one config-2
     factorization, from the committed ncu capture (``ncu --metrics dram__bytes_read.sum,
     dram__bytes_write.sum -k regex:panel_cluster python tools/run_blk.py --reps 1``; the
