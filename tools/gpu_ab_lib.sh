@@ -16,3 +16,6 @@ for L in $OLD $NEW; do
   echo "$(basename $L) $(SKEWLTL_B200_LIB=$L timeout 300 python tools/time_batched.py 2>&1 | tail -2 | tr '\n' ' ')" >> gpurun_out/ab.log
 done
 timeout 600 python -m pytest tests/test_gpu_batched.py -x -q -m gpu > gpurun_out/ab_tests_b.log 2>&1; echo "rc=$?" >> gpurun_out/ab_tests_b.log
+SKEWLTL_B200_LIB=$OLD timeout 300 python tools/bitcmp.py /tmp/bc_old.npz
+SKEWLTL_B200_LIB=$NEW timeout 300 python tools/bitcmp.py /tmp/bc_new.npz
+python tools/bitcmp.py /tmp/bc_old.npz /tmp/bc_new.npz >> gpurun_out/ab.log 2>&1
