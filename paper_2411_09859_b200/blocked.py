@@ -107,6 +107,19 @@ def _check_block(b):
         raise ValueError("block size must be >= 1")
 
 
+def _check_out_device(x, m, L, tau, piv):
+    """out=(L, tau, piv) buffers cross the C ABI as raw pointers: check them here."""
+    t = dv.torch()
+    if not (dv.is_colmajor_cuda(L) and L.dtype == t.float64 and tuple(L.shape) == (m, m) and L.device == x.device):
+        raise ValueError("out L must be a column-major float64 (m, m) CUDA tensor on x's device")
+    for name, v, dt, size in (("tau", tau, t.float64, m - 1), ("piv", piv, t.int64, m)):
+        if v is None and name == "piv":
+            continue
+        if not (dv._is_cuda_tensor(v) and v.dtype == dt and v.dim() == 1 and v.numel() >= size
+                and v.is_contiguous() and v.device == x.device):
+            raise ValueError(f"out {name} must be a contiguous {dt} CUDA tensor of length {size} on x's device")
+
+
 def ltlt_blk_piv_device(x, b=DEFAULT_BLOCK, fused="var1", out=None, stream=None):
     """Device-resident entry: ``x`` is a column-major float64 CUDA tensor.
 
@@ -129,12 +142,13 @@ def ltlt_blk_piv_device(x, b=DEFAULT_BLOCK, fused="var1", out=None, stream=None)
         piv = t.empty(m, dtype=t.int64, device=x.device)
     else:
         L, tau, piv = out
+        _check_out_device(x, m, L, tau, piv)
     lib = _capi.load()
     code = _capi.VARIANT_CODES[fused]
     nbytes = lib.skl_ltlt_blk_piv_workspace_size(m, int(b), code)
     if nbytes == 0:
         raise InvalidVariant("configuration not supported by the GPU panel kernel")
-    ws = dv.workspace(nbytes)
+    ws = dv.workspace(nbytes, stream=stream)
     st = lib.skl_ltlt_blk_piv(m, int(b), code, x.data_ptr(), dv.ld_of(x), L.data_ptr(), dv.ld_of(L),
                               tau.data_ptr() if m > 1 else None, piv.data_ptr(), ws.data_ptr(), nbytes,
                               dv.stream_ptr(stream))
@@ -167,14 +181,20 @@ def ltlt_blk_piv_host(x, b=DEFAULT_BLOCK, fused="var1", out=None, stream=None, s
         piv = np.empty(m, dtype=np.int64)
     else:
         L, tau, piv = out
-        if not (L.flags.f_contiguous and L.dtype == np.float64 and L.shape == (m, m)):
+        if not (isinstance(L, np.ndarray) and L.flags.f_contiguous and L.dtype == np.float64 and L.shape == (m, m)):
             raise ValueError("out L must be an F-ordered float64 (m, m) array")
+        if not (isinstance(tau, np.ndarray) and tau.dtype == np.float64 and tau.ndim == 1
+                and tau.size >= m - 1 and tau.flags.c_contiguous):
+            raise ValueError("out tau must be a contiguous float64 array of length m - 1")
+        if not (isinstance(piv, np.ndarray) and piv.dtype == np.int64 and piv.ndim == 1
+                and piv.size >= m and piv.flags.c_contiguous):
+            raise ValueError("out piv must be a contiguous int64 array of length m")
     lib = _capi.load()
     code = _capi.VARIANT_CODES[fused]
     nbytes = lib.skl_ltlt_blk_piv_host_workspace_size(m, int(b), code)
     if nbytes == 0:
         raise InvalidVariant("configuration not supported by the GPU panel kernel")
-    ws = dv.workspace(nbytes)
+    ws = dv.workspace(nbytes, stream=stream)
     st = lib.skl_ltlt_blk_piv_host(m, int(b), code, x.ctypes.data, m, L.ctypes.data, m,
                                    tau.ctypes.data if m > 1 else None, piv.ctypes.data, ws.data_ptr(), nbytes,
                                    dv.stream_ptr(stream))
@@ -193,6 +213,9 @@ def ltlt_blk_piv(x: SkewMatrixLower, b=DEFAULT_BLOCK, fused="var1", features=Non
     if fused not in PIVOTED_FUSED:
         raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
     _check_block(b)
+    if fused != "var1" and features is not None and not features.external_t:
+        # blocked.py:326-327: the fused pivoted schedules need tau in an external vector
+        raise InvalidVariant(f"pivoted blk-{fused} needs tau in an external vector (external_t)")
     if not isinstance(x, SkewMatrixLower):
         x = SkewMatrixLower(x)
     m = x.m
@@ -249,6 +272,7 @@ def ltlt_blk_device(x, b=DEFAULT_BLOCK, fused="var1", pivot=False, out=None, str
         tau = t.empty(max(m - 1, 0), dtype=t.float64, device=x.device)
     else:
         L, tau = out
+        _check_out_device(x, m, L, tau, None)
     piv = t.empty(m, dtype=t.int64, device=x.device) if pivot else None
     info = t.zeros(1, dtype=t.int32, device=x.device)
     lib = _capi.load()
@@ -256,7 +280,7 @@ def ltlt_blk_device(x, b=DEFAULT_BLOCK, fused="var1", pivot=False, out=None, str
     nbytes = lib.skl_ltlt_blk_piv_workspace_size(m, int(b), code)
     if nbytes == 0:
         raise InvalidVariant("configuration not supported by the GPU panel kernel")
-    ws = dv.workspace(nbytes)
+    ws = dv.workspace(nbytes, stream=stream)
     st = lib.skl_ltlt_blk(m, int(b), code, 1 if pivot else 0, x.data_ptr(), dv.ld_of(x), L.data_ptr(), dv.ld_of(L),
                           tau.data_ptr() if m > 1 else None, piv.data_ptr() if pivot else None, info.data_ptr(),
                           ws.data_ptr(), nbytes, dv.stream_ptr(stream))

@@ -12,6 +12,8 @@
 // then applied to every right-hand side in parallel (back substitution by the
 // reciprocal pivots).
 #include <cfloat>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -410,6 +412,49 @@ size_t solve_workspace_bytes(int n, int nrhs) {
          al(sizeof(int) * n);
 }
 
+namespace {
+// per-device side stream for the overlapped tridiagonal factorization
+cudaError_t side_stream_for(cudaStream_t stream, cudaStream_t* out) {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> sides;
+  int dev = 0;
+  cudaError_t err = cudaStreamGetDevice(stream, &dev);
+  if (err != cudaSuccess) return err;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = sides.find(dev);
+  if (it != sides.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  int cur = 0;
+  if ((err = cudaGetDevice(&cur)) != cudaSuccess) return err;
+  if (cur != dev && (err = cudaSetDevice(dev)) != cudaSuccess) return err;
+  cudaStream_t s = nullptr;
+  err = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (cur != dev) cudaSetDevice(cur);
+  if (err != cudaSuccess) return err;
+  sides[dev] = s;
+  *out = s;
+  return cudaSuccess;
+}
+
+// fork/join events owned by one call; destroyed when the call returns (CUDA
+// releases them once the recorded work has completed)
+struct EventPair {
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaError_t create() {
+    cudaError_t e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+    return e;
+  }
+  ~EventPair() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
+};
+
+}  // namespace
+
 cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const double* tau, const long long* piv,
                          double* B, long long ldb, double tol_scale, int* info, void* ws, cudaStream_t stream) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
@@ -454,13 +499,13 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
   // the tridiagonal factorization depends on tau only: it runs on a side stream,
   // overlapped with the permutation and the forward sweep (one thread's sequential
   // recurrence, ~0.6 ms at n = 4096, would otherwise sit on the critical path)
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (side == nullptr) {
-    if ((err = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking)) != cudaSuccess) return err;
-    if ((err = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming)) != cudaSuccess) return err;
-    if ((err = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming)) != cudaSuccess) return err;
-  }
+  // one side stream per device (the caller's stream's device, not the current one);
+  // the fork/join events are per call, so concurrent calls never wait on each other's
+  cudaStream_t side = nullptr;
+  if ((err = side_stream_for(stream, &side)) != cudaSuccess) return err;
+  EventPair evs;
+  if ((err = evs.create()) != cudaSuccess) return err;
+  cudaEvent_t ev_fork = evs.fork, ev_join = evs.join;
   if ((err = cudaEventRecord(ev_fork, stream)) != cudaSuccess) return err;  // info zeroed, inputs ready
   if ((err = cudaStreamWaitEvent(side, ev_fork, 0)) != cudaSuccess) return err;
   tridiag_factor_kernel<<<1, 256, 0, side>>>(n, tau, tol_scale, d, e, f2, mult, swp, info);

@@ -33,14 +33,27 @@ def stream_ptr(stream=None):
     return s.cuda_stream
 
 
-def workspace(nbytes, device=None):
-    """Grow-only per-device scratch buffer (uint8 tensor)."""
+def workspace(nbytes, device=None, stream=None):
+    """Grow-only scratch buffer (uint8 tensor), one per (device, stream).
+
+    Calls enqueued on different streams never share scratch.  When a buffer
+    grows, the old one is handed back to the caching allocator only after the
+    work already queued on its stream has finished (``record_stream``).
+    """
     t = torch()
-    dev = t.device("cuda", t.cuda.current_device() if device is None else device)
-    buf = _WS.get(dev)
-    if buf is None or buf.numel() < nbytes:
-        buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=dev)
-        _WS[dev] = buf
+    if stream is not None:
+        dev = stream.device
+    else:
+        dev = t.device("cuda", t.cuda.current_device() if device is None else device)
+    with t.cuda.device(dev):
+        st = stream if stream is not None else t.cuda.current_stream(dev)
+        key = (dev, st.cuda_stream)
+        buf = _WS.get(key)
+        if buf is None or buf.numel() < nbytes:
+            if buf is not None:
+                buf.record_stream(st)
+            buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=dev)
+            _WS[key] = buf
     return buf
 
 

@@ -48,10 +48,12 @@ def ltlt_unb_twostep_device(xd, pivot=False, out=None, stream=None):
         piv = t.zeros(m, dtype=t.int64, device="cuda")
     else:
         L, tau, piv = out
+        from .blocked import _check_out_device
+        _check_out_device(xd, m, L, tau, piv)
     info = t.zeros(1, dtype=t.int32, device="cuda")
     lib = _capi.load()
     nbytes = lib.skl_ltlt_unb_twostep_workspace_size(m)
-    ws = dv.workspace(nbytes)
+    ws = dv.workspace(nbytes, stream=stream)
     st = lib.skl_ltlt_unb_twostep(m, 1 if pivot else 0, xd.data_ptr(), dv.ld_of(xd), L.data_ptr(), dv.ld_of(L),
                                   tau.data_ptr() if m > 1 else None, piv.data_ptr(), info.data_ptr(),
                                   ws.data_ptr(), nbytes, dv.stream_ptr(stream))
