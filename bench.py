@@ -41,6 +41,29 @@ SKR2K_FLOPS = 4 * 64 * (N * (N - 1) // 2)  # kernels3.py:323 with keff = 64
 METRIC = "LTL^T factorization GFLOP/s (n^3/3) and % of FP64 peak; skr2k GFLOP/s"
 
 
+def headline_config(world):
+    """The `config` object of BOTH arms (ours and --impl reference)."""
+    cfg = {"workload": f"blocked pivoted LTL^T n={N} nb={NB} {FUSED} (BASELINE configs[1])", "n": N, "nb": NB,
+           "fused": FUSED, "input": "X=G-G^T, G~N(0,1) Philox seed 0 (replica r of N>1 ranks: seed r)",
+           "parallelism": "replicas" if world > 1 else "single",
+           "l2": "flushed (256 MB write) between timed steps"}
+    cfg["gpu_panel_width"] = gpu_panel_width()
+    return cfg
+
+
+def gpu_panel_width():
+    """GPU panel schedule at config 2 (the reference's nb accounting is kept for
+    the flop tallies; the GPU panel can be narrower than nb)."""
+    try:
+        from paper_2411_09859_b200.blocked import gpu_panel_plan
+        plan = gpu_panel_plan(N, NB, FUSED)
+    except Exception as exc:  # noqa: BLE001 -- no device in this process
+        return f"unavailable ({type(exc).__name__})"
+    widths = [p["nelim"] for p in plan]
+    return {"panels": len(plan), "max": max(widths), "first": widths[0], "last": widths[-1],
+            "kinds": sorted({f"{p['kind']}x{p['ctas']}" for p in plan})}
+
+
 def dist_setup(gpus):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -159,7 +182,7 @@ def _time(torch, fn, reps, e0, e1, flush=None):
     return statistics.median(out)
 
 
-def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush):
+def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush, rows5):
     """Configs 1, 3, 4 of BASELINE.json on this GPU (device-resident inputs)."""
     from paper_2411_09859_b200 import apps
     from paper_2411_09859_b200.inputs import skew_lower
@@ -195,7 +218,7 @@ def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush):
     t3 = torch.empty(16383, dtype=torch.float64, device="cuda")
     p3 = torch.empty(16384, dtype=torch.int64, device="cuda")
     pk.ltlt_blk_piv_device(x3, 256, "var1", out=(L3, t3, p3))
-    ms = _time(torch, lambda: pk.ltlt_blk_piv_device(x3, 256, "var1", out=(L3, t3, p3)), 2, e0, e1, flush)
+    ms = _time(torch, lambda: pk.ltlt_blk_piv_device(x3, 256, "var1", out=(L3, t3, p3)), 3, e0, e1, flush)
     g3 = 16384 ** 3 / 3 / (ms * 1e-3) / 1e9
     res["config3_blk_piv_n16384_nb256"] = {"ms": round(ms, 2), "gflops": round(g3, 1),
                                            "pct_fp64_peak": round(100 * g3 / 1e3 / fp64_peak, 2)}
@@ -213,7 +236,8 @@ def other_configs(torch, pk, dv, fp64_peak, e0, e1, flush):
         del xd
     torch.cuda.empty_cache()
     # config 5 on one GPU (the distributed driver runs under torchrun, N > 1)
-    res["config5_blk_piv_n49152_nb512"] = config5_single(torch, pk, dv, fp64_peak, e0, e1)
+    torch.cuda.empty_cache()
+    res["config5_blk_piv_n49152_nb512"] = config5_single(torch, pk, dv, fp64_peak, e0, e1, rows5)
     return res
 
 
@@ -221,37 +245,55 @@ N5, NB5 = 49152, 512
 FLOPS5 = N5 ** 3 / 3.0
 
 
-def config5_input(torch, n=N5, seed=0):
-    """Config 5 input on the device: X = G - G^T, G iid N(0, 1/n) (torch's CUDA
-    Philox generator, seed 0 -- the same matrix on every rank).  Parity at this
-    size is property-based (tools/run_cfg5.py: residual, log|Pf| = slogdet/2),
-    so the bench skips the 35 s host Philox draw."""
-    gen = torch.Generator(device="cuda")
-    gen.manual_seed(seed)
-    G = torch.randn((n, n), generator=gen, dtype=torch.float64, device="cuda")
-    G /= n ** 0.5
-    X = torch.empty((n, n), dtype=torch.float64, device="cuda").t()
-    for j0 in range(0, n, 4096):
-        X[:, j0:j0 + 4096] = G[:, j0:j0 + 4096] - G[j0:j0 + 4096, :].t()
-    del G
-    torch.cuda.empty_cache()
-    return X
+class Config5Rows:
+    """Config 5's G (BASELINE Philox seed 0, N(0, 1/n)) drawn on the host in a
+    background thread while the other configs run on the GPU (numpy releases the
+    GIL in its fills; ~40 s of one host core).  The same matrix the reference
+    golden tests/golden/cfg5_n49152_b512.npz was computed from."""
+
+    def __init__(self, n=N5, seed=0):
+        self.n, self.seed, self.g, self.err = n, seed, None, None
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        try:
+            from paper_2411_09859_b200.inputs import normal_scaled_rows
+            self.g = normal_scaled_rows(self.n, self.seed)
+        except Exception as exc:  # noqa: BLE001 -- re-raised in get()
+            self.err = exc
+
+    def get(self):
+        self.thread.join()
+        if self.err is not None:
+            raise self.err
+        return self.g
 
 
-def config5_single(torch, pk, dv, fp64_peak, e0, e1):
+def config5_input(torch, rows):
+    """Config 5 input on the device: X = G - G^T from the host-drawn rows."""
+    from paper_2411_09859_b200.inputs import skew_device_from_rows
+    x = skew_device_from_rows(rows.get(), torch)
+    rows.g = None
+    return x
+
+
+def config5_single(torch, pk, dv, fp64_peak, e0, e1, rows):
     """Config 5 (n=49152, nb=512) on ONE GPU through the single-device driver."""
-    X = config5_input(torch)
+    X = config5_input(torch, rows)
     L = dv.empty_colmajor(N5, N5, torch.float64)
     t5 = torch.empty(N5 - 1, dtype=torch.float64, device="cuda")
     p5 = torch.empty(N5, dtype=torch.int64, device="cuda")
     pk.ltlt_blk_piv_device(X, NB5, "var1", out=(L, t5, p5))
-    ms = _time(torch, lambda: pk.ltlt_blk_piv_device(X, NB5, "var1", out=(L, t5, p5)), 2, e0, e1)
+    ms = _time(torch, lambda: pk.ltlt_blk_piv_device(X, NB5, "var1", out=(L, t5, p5)), 3, e0, e1)
     g5 = FLOPS5 / (ms * 1e-3) / 1e9
+    piv = p5.cpu().numpy()
     del X, L
     dv._WS.clear()
     torch.cuda.empty_cache()
     return {"ms": round(ms, 1), "gflops": round(g5, 1), "pct_fp64_peak": round(100 * g5 / 1e3 / fp64_peak, 2),
-            "input": "X=G-G^T, G~N(0,1/n) torch CUDA generator seed 0 (device-generated)"}
+            "reps": 3, "input": "X=G-G^T, G=Philox(0).standard_normal((n,n))/sqrt(n) (BASELINE; host-drawn)",
+            "nontrivial_pivots": int(np.count_nonzero(piv))}
 
 
 def config4_sharded(torch, world, rank):
@@ -289,11 +331,11 @@ def config4_sharded(torch, world, rank):
     return out
 
 
-def config5_distributed(torch, world, rank, fp64_peak):
+def config5_distributed(torch, world, rank, fp64_peak, rows):
     """Config 5 over the N ranks: block-cyclic columns (nbd=512), VMM-mapped peer
     blocks, NCCL stream barrier (skl_ltlt_blk_piv_dist).  Device time, max over ranks."""
     from paper_2411_09859_b200.dist import DistLTLT
-    X = config5_input(torch)
+    X = config5_input(torch, rows)
     ctx = DistLTLT(N5, NB5, "var1", nbd=512, barrier="nccl")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
@@ -318,14 +360,19 @@ def config5_distributed(torch, world, rank, fp64_peak):
             "nontrivial_pivots": int(np.count_nonzero(piv)), "scaling": "strong (one matrix)"}
 
 
-def cpu_baseline_port(x, budget_s=30.0):
-    """The oracle (NumPy restatement of the reference) on the host cores."""
+def cpu_baseline_port(x, reps=3, budget_s=30.0):
+    """The oracle (NumPy restatement of the reference) on the host cores: median
+    of `reps` full config-2 factorizations (fewer if one takes over budget_s/reps)."""
     import oracle
-    t0 = time.perf_counter()
-    oracle.ltlt_blk_piv(x, b=NB, fused=FUSED)
-    dt = time.perf_counter() - t0
-    reps = 1
-    return FLOPS / dt / 1e9, reps, dt
+    times = []
+    while len(times) < reps:
+        t0 = time.perf_counter()
+        oracle.ltlt_blk_piv(x, b=NB, fused=FUSED)
+        times.append(time.perf_counter() - t0)
+        if sum(times) > budget_s and len(times) >= 1:
+            break
+    dt = statistics.median(times)
+    return FLOPS / dt / 1e9, len(times), dt
 
 
 def run_reference(args, world, rank):
@@ -358,8 +405,7 @@ def run_reference(args, world, rank):
     line = {"metric": METRIC, "value": round(val, 3), "unit": "GFLOP/s", "impl": "reference", "n_gpus": 0,
             "steps": len(times), "warmup": len(t_w), "ms_per_step": round(ms, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"blocked pivoted LTL^T n={N} nb={NB} {FUSED}", "n": N, "nb": NB,
-                       "fused": FUSED, "input": "X=G-G^T, G~N(0,1) Philox seed 0"},
+            "config": headline_config(world),
             "cpu_baseline": {"value": round(val, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": round(val, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -414,6 +460,7 @@ def main():
 
     torch.cuda.set_device(local)
     lib = _capi.load()
+    rows5 = None if args.skip_other else Config5Rows()   # host draw overlaps the GPU timing below
     x = skew_lower(N, rank)  # each replica factors its own matrix (rank 0: the config's seed 0)
     x_pin = torch.empty((N, N), dtype=torch.float64).pin_memory()
     x_pin.copy_(torch.from_numpy(np.ascontiguousarray(x.T)))  # (cols, rows) row-major == column-major X
@@ -536,16 +583,13 @@ def main():
     # ---- the other BASELINE configs (secondary; not the headline value) ---------------
     other = {}
     if not args.skip_other and world == 1:
-        other = other_configs(torch, pk, dv, fp64_peak, e0, e1, flush)
+        other = other_configs(torch, pk, dv, fp64_peak, e0, e1, flush, rows5)
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"blocked pivoted LTL^T n={N} nb={NB} {FUSED} (BASELINE configs[1])", "n": N,
-                   "nb": NB, "fused": FUSED, "input": "X=G-G^T, G~N(0,1) Philox seed rank",
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "flushed (256 MB write) between timed steps"},
+        "config": headline_config(world),
         "pct_fp64_peak": round(100 * value / world / 1e3 / fp64_peak, 2),
         "fp64_peak_tflops": round(fp64_peak, 2),
         "skr2k": {"value": round(skr, 1), "unit": "GFLOP/s", "flops": SKR2K_FLOPS,
@@ -563,7 +607,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         val, reps, dt = cpu_baseline_port(x)
         line["cpu_baseline"] = {"value": round(val, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"{reps} full factorization of config 2 by the oracle port ({dt:.1f} s)"}
+                                "sample": f"median of {reps} full factorizations of config 2 by the oracle port "
+                                          f"({dt:.1f} s each), OpenBLAS on all host threads"}
     if world > 1 and not args.skip_other:
         # config 5 across the ranks; a watchdog prints the line without it if the
         # distributed run does not finish (never leave the driver's run hanging)
@@ -582,7 +627,8 @@ def main():
         try:
             del flush
             torch.cuda.empty_cache()
-            line["other_configs"]["config5_dist_n49152_nb512"] = config5_distributed(torch, world, rank, fp64_peak)
+            line["other_configs"]["config5_dist_n49152_nb512"] = config5_distributed(torch, world, rank, fp64_peak,
+                                                                                      rows5)
         except Exception as exc:  # noqa: BLE001 -- reported in the line
             line["other_configs"]["config5_dist_n49152_nb512"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
         timer.cancel()

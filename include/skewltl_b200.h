@@ -118,6 +118,14 @@ int skl_unpack_factor(int n, const double* X, long long ldx, double* L, long lon
  *   from X.  tau (n-1) and piv (n, int64 relative offsets, piv[0] = 0) are
  *   device outputs.  variant: SKL_VAR1 / SKL_VAR2A / SKL_VAR2B.             */
 size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant);
+/* GPU panel schedule of skl_ltlt_blk_piv (a query, no device work): the panel
+ *   width on the GPU may be narrower than nb when the panel block would not fit
+ *   on-chip (the factorization is invariant to it).  Writes up to cap entries
+ *   r[i] (first column), nelim[i] (columns eliminated), kind[i] (2: cluster
+ *   panel, ctas[i] CTAs in clusters of csize[i]; 0: grid-wide panel); returns
+ *   the number of panels, or -1 when the configuration is unsupported.      */
+int skl_ltlt_blk_piv_plan(int n, int nb, int variant, int* r, int* nelim, int* kind, int* ctas, int* csize,
+                          int cap);
 int skl_ltlt_blk_piv(int n, int nb, int variant, const double* X, long long ldx, double* L, long long ldl,
                      double* tau, long long* piv, void* workspace, size_t workspace_bytes, void* stream);
 

@@ -41,6 +41,7 @@ SIGNATURES = {
     "skl_pack_factor": (_i, [_i, _p, _ll, _p, _p, _ll, _p]),
     "skl_unpack_factor": (_i, [_i, _p, _ll, _p, _ll, _p, _p]),
     "skl_ltlt_blk_piv_workspace_size": (_sz, [_i, _i, _i]),
+    "skl_ltlt_blk_piv_plan": (_i, [_i, _i, _i, _p, _p, _p, _p, _p, _i]),
     "skl_ltlt_blk_piv": (_i, [_i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _sz, _p]),
     "skl_ltlt_blk": (_i, [_i, _i, _i, _i, _p, _ll, _p, _ll, _p, _p, _p, _p, _sz, _p]),
     "skl_ltlt_unb_panel_workspace_size": (_sz, [_i, _i]),

@@ -107,6 +107,26 @@ def _check_block(b):
         raise ValueError("block size must be >= 1")
 
 
+def gpu_panel_plan(m, b=DEFAULT_BLOCK, fused="var1"):
+    """The GPU panel schedule of ltlt_blk_piv for (m, b, fused): one dict per panel
+    (first column r, columns eliminated, kind "cluster"/"grid", CTAs, cluster size).
+    The GPU panel width can be narrower than b when the panel block would not fit
+    on-chip; pivots, L and T are invariant to it."""
+    import ctypes as C
+    if fused not in PIVOTED_FUSED:
+        raise InvalidVariant(f"fused must be one of {PIVOTED_FUSED}, got {fused!r}")
+    dv.require_cuda()
+    lib = _capi.load()
+    cap = max(int(m), 1)
+    bufs = [(C.c_int * cap)() for _ in range(5)]
+    cnt = lib.skl_ltlt_blk_piv_plan(int(m), int(b), _capi.VARIANT_CODES[fused], *bufs, cap)
+    if cnt < 0:
+        raise InvalidVariant("configuration not supported by the GPU panel kernel")
+    r, ne, kind, ctas, cs = (list(v)[:cnt] for v in bufs)
+    return [{"r": r[i], "nelim": ne[i], "kind": "cluster" if kind[i] else "grid", "ctas": ctas[i],
+             "cluster_size": cs[i]} for i in range(cnt)]
+
+
 def _check_out_device(x, m, L, tau, piv):
     """out=(L, tau, piv) buffers cross the C ABI as raw pointers: check them here."""
     t = dv.torch()

@@ -555,6 +555,21 @@ size_t skl_ltlt_blk_piv_workspace_size(int n, int nb, int variant) {
   return layout_blk(n, nb, plan, nullptr, nullptr, left);
 }
 
+int skl_ltlt_blk_piv_plan(int n, int nb, int variant, int* r, int* nelim, int* kind, int* ctas, int* csize,
+                          int cap) {
+  if (n < 1 || nb < 1 || variant < SKL_VAR1 || variant > SKL_VAR2B) return -1;
+  std::vector<PanelPlan> plan;
+  if (!make_schedule(n, nb, variant, plan)) return -1;
+  for (int i = 0; i < (int)plan.size() && i < cap; ++i) {
+    if (r) r[i] = plan[i].r;
+    if (nelim) nelim[i] = plan[i].nelim;
+    if (kind) kind[i] = plan[i].cluster;
+    if (ctas) ctas[i] = plan[i].ctas;
+    if (csize) csize[i] = plan[i].csize;
+  }
+  return (int)plan.size();
+}
+
 namespace {
 // blocked driver behind skl_ltlt_blk_piv / skl_ltlt_blk / skl_ltlt_unb_panel:
 // eliminates columns [0, ncols); pivot = 0 runs the unpivoted drivers (pivot row

@@ -137,6 +137,19 @@ __device__ __forceinline__ void mbar_wait_acq_cluster(uint64_t* bar, uint32_t pa
       : "memory");
 }
 
+// wait for a phase whose payload was delivered into THIS CTA's shared memory by
+// st.async / bulk copies completing on the barrier (complete_tx): the bytes are
+// in local smem once the phase flips, so a CTA-scope acquire is enough (the
+// cluster-scope form compiles to an extra CCTL.IVALL -- an L1 invalidate -- per
+// wait).  SKL_XBAR_ACQ_CLUSTER=1 restores the cluster-scope wait (A/B builds).
+__device__ __forceinline__ void mbar_wait_delivered(uint64_t* bar, uint32_t parity) {
+#if defined(SKL_XBAR_ACQ_CLUSTER) && SKL_XBAR_ACQ_CLUSTER
+  mbar_wait_acq_cluster(bar, parity);
+#else
+  mbar_wait(bar, parity);
+#endif
+}
+
 // global -> shared bulk copy, completion signalled on `bar` (bytes multiple of 16)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         if (warp == 1 && lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
       }
       CMARK(1);
-      mbar_wait_acq_cluster(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
+      mbar_wait_delivered(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
     } else {
       if (warp == 0) {
         const bool ok = lane < kCWarps && s.wcand[lane].idx >= 0;
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
           for (int j = lane; j <= k; j += 32) ll_put_double(ra + 4 + 2 * j, s.slab[(size_t)j * Rs + la], tag);
           if (lane == 0) ll_put2(ra, uint32_t(s.perm[la]), 0u, tag);
         }
-        mbar_wait_acq_cluster(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
+        mbar_wait_delivered(&s.xbar[par], (uint32_t(g - r) >> 1) & 1u);
       } else {
         cluster_barrier();
       }
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
         (void)oo;
         if (lane < C) st_async_cand(s.gwin + par, &s.xbar[2 + par], lane, gw);
       }
-      mbar_wait_acq_cluster(&s.xbar[2 + par], (uint32_t(g - r) >> 1) & 1u);
+      mbar_wait_delivered(&s.xbar[2 + par], (uint32_t(g - r) >> 1) & 1u);
       w = s.gwin[par];
       owner = w.idx >= 0 ? (w.idx - row0) / R : 0;  // rows are dealt out contiguously
     }
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kCThreads, 1) panel_cluster_kernel(PanelArgs a
     SUBMARK(1);
     if (push) {
       // the winner's row (pushed with its candidate) is read in place by phase 4
-      mbar_wait_acq_cluster(&s.xbar[2 + par], (uint32_t(g - r) >> 1) & 1u);
+      mbar_wait_delivered(&s.xbar[2 + par], (uint32_t(g - r) >> 1) & 1u);
       xrow = s.crows + ((size_t)par * C + owner) * CRS;
     } else if (MULTI) {
       const uint64_t* gr = a.pivot ? a.slots + ((size_t)owner * 2 + par) * a.slot_words + 4
@@ -840,6 +840,475 @@ cudaError_t launch_panel_finish(const PanelArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// panel_push_kernel: the single-cluster pivoted panel, rebuilt for the shortest
+// per-elimination dependency chain (configs 1 and 2, and the tail panels of
+// configs 3 and 5).  Same reference semantics and outputs as the push mode of
+// panel_cluster_kernel<true> (lazy interchanges: slab rows never move, a row
+// carries its position as a label), but:
+//  * every per-row quantity lives in registers of the owning thread (label,
+//    physical row, the next column's value, A z, this step's v), so the step
+//    touches shared memory only for the slab columns, the candidates and z;
+//  * the CTA candidate and the winner are found by every warp redundantly
+//    (one exact 3-redux argmax each), so a step has exactly two CTA barriers;
+//  * remote addresses (candidate slots, row slots, mbarriers of every peer)
+//    are computed once (mapa) before the step loop;
+//  * the candidate row push is laid out as (destination = tid % 16, pair =
+//    tid / 16), so no integer division sits on the step;
+//  * the column scaling v / vb runs on the value still in a register, in the
+//    shadow of the pushed-row wait and the z barrier, and the gemv reads the
+//    freshly scaled column k from that register;
+//  * slab columns [0, 32 * NBANK) of a thread's row are register-cached.
+// ===========================================================================
+constexpr int kPThreads = 256;
+constexpr int kPWarps = kPThreads / 32;
+constexpr int kPC = 16;  // cluster size of the push panel
+
+struct __align__(16) PCand {  // pushed to every CTA of the cluster
+  double v;
+  int pos;
+  int ph;
+};
+struct __align__(16) PWCand {  // CTA-local warp candidate
+  double v;
+  int pos;
+  int ph;
+  int li;
+  int pad[3];
+};
+
+__host__ __device__ inline int push_crs(int kmax) { return (kmax + 2) & ~1; }  // even -> 16-byte rows
+
+struct PSmem {
+  double* slab;   // [kmax][Rs]
+  double* crows;  // [2][16][CRS]
+  double* zbuf;   // [kmax + 2]
+  double* taus;   // [kmax + 2]
+  PCand* cand;    // [2][16]
+  PWCand* wcand;  // [8]
+  int* pivbuf;    // [kmax]
+  uint64_t* xbar; // [4]: candidates (par), rows (2 + par)
+};
+
+__host__ __device__ inline size_t psmem_layout(int R, int kmax, PSmem* s, unsigned char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 15) & ~size_t(15);
+    return base ? base + o : nullptr;
+  };
+  const int Rs = cslab_stride(R);
+  unsigned char* p;
+  p = take(sizeof(double) * (size_t)kmax * Rs);
+  if (s) s->slab = (double*)p;
+  p = take(sizeof(double) * 2 * kPC * (size_t)push_crs(kmax));
+  if (s) s->crows = (double*)p;
+  p = take(sizeof(double) * (kmax + 2));
+  if (s) s->zbuf = (double*)p;
+  p = take(sizeof(double) * (kmax + 2));
+  if (s) s->taus = (double*)p;
+  p = take(sizeof(PCand) * 2 * kPC);
+  if (s) s->cand = (PCand*)p;
+  p = take(sizeof(PWCand) * kPWarps);
+  if (s) s->wcand = (PWCand*)p;
+  p = take(sizeof(int) * (kmax + 2));
+  if (s) s->pivbuf = (int*)p;
+  p = take(sizeof(uint64_t) * 4);
+  if (s) s->xbar = (uint64_t*)p;
+  return off;
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t rdst, uint32_t rbar, uint32_t a, uint32_t b, uint32_t c,
+                                            uint32_t d) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   rdst),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2f64(uint32_t rdst, uint32_t rbar, double x, double y) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(rdst),
+               "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
+
+// exact argmax of |v| over the lanes (ties -> lowest pos); returns the winning lane or -1.
+// Fast path: one redux on the top 32 bits of |v| (+1, so a valid 0.0 beats an empty
+// lane); when exactly one lane holds that top word it is the maximum.  Otherwise the
+// low words and then the positions decide among the tied lanes (two more reduxes).
+__device__ __forceinline__ int lane_argmax(double v, int pos, bool valid) {
+  const unsigned long long bits = valid ? (unsigned long long)__double_as_longlong(fabs(v)) : 0ull;
+  const unsigned hi = valid ? unsigned(bits >> 32) + 1u : 0u;
+  const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+  if (m1 == 0u) return -1;
+  const bool c1 = hi == m1;
+  const unsigned b1 = __ballot_sync(0xffffffffu, c1);
+  if ((b1 & (b1 - 1u)) == 0u) return __ffs(b1) - 1;
+  const unsigned lo = unsigned(bits);
+  const unsigned m2 = __reduce_max_sync(0xffffffffu, c1 ? lo : 0u);
+  const bool c2 = c1 && lo == m2;
+  const unsigned id = __reduce_min_sync(0xffffffffu, c2 ? unsigned(pos) : 0xffffffffu);
+  return __ffs(__ballot_sync(0xffffffffu, c2 && unsigned(pos) == id)) - 1;
+}
+
+// RPT rows per thread (TPR == 1), or TPR threads per row (RPT == 1): the TPR threads of a
+// row are consecutive lanes; they hold the row's state redundantly and split the gemv's
+// columns (j % TPR == part), combining the partial sums with xor-shuffles.  NBANK banks
+// of 32 slab columns are register-cached (each of the TPR threads caches its 32/TPR).
+template <int RPT, int NBANK, int TPR, bool MCAST>
+__global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
+  static_assert(RPT == 1 || TPR == 1, "either rows per thread or threads per row");
+  constexpr int RPB = kPThreads / TPR;   // rows per row-block of the CTA's threads
+  constexpr int CPB = 32 / TPR;          // cached columns per bank and thread
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int crank = int(cg::this_cluster().block_rank());
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int part = TPR > 1 ? (tid & (TPR - 1)) : 0;
+  const int rowt = TPR > 1 ? tid / TPR : tid;  // this thread's (first) local row
+  const int n = a.n, lo = a.lo, r = a.r, nelim = a.nelim, kmax = a.kmax;
+  const int R = a.rows_per, Rs = cslab_stride(R);
+  const long long ld = a.ld;
+  const double* __restrict__ W = a.W;
+  const int row0 = lo + 1;
+  const int rbase = row0 + crank * R;
+  const int rcount = max(0, min(R, n - rbase));
+  const int rt = r + nelim;
+  const int CRS = push_crs(kmax);
+  PSmem s;
+  psmem_layout(R, kmax, &s, smem_raw);
+
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);
+    fence_mbar_init();
+  }
+  for (int j = tid; j < kmax + 2; j += kPThreads) {
+    s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
+    s.zbuf[j] = 0.0;
+  }
+  // per-row state in registers: row li = rowt + u * RPB
+  int lab[RPT], ph[RPT];
+  double cn[RPT], az[RPT], vv[RPT];
+  bool cneg[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int li = rowt + u * RPB;
+    const int pos = rbase + li;
+    lab[u] = li < rcount ? pos : -1;  // -1: no row (never a candidate, never written)
+    ph[u] = pos;
+    az[u] = 0.0;
+    vv[u] = 0.0;
+    cneg[u] = false;
+    cn[u] = (li < rcount && pos > r) ? W[(long long)r * ld + pos] : 0.0;
+    if (part == 0 && li < rcount && lo < r) s.slab[li] = W[(long long)lo * ld + pos];  // var2a carry column
+  }
+  double rb[RPT][CPB * NBANK];
+  int nbank = 0;
+  // remote addresses, fixed for the whole panel
+  const uint32_t dst = uint32_t(tid & (kPC - 1));
+  const uint32_t r_crows = mapa_u32(smem_u32(s.crows), dst);
+  const uint32_t r_rbar0 = mapa_u32(smem_u32(&s.xbar[2]), dst);
+  const uint32_t r_rbar1 = mapa_u32(smem_u32(&s.xbar[3]), dst);
+  const uint32_t r_cand = mapa_u32(smem_u32(s.cand), uint32_t(lane & (kPC - 1)));
+  const uint32_t r_cbar0 = mapa_u32(smem_u32(&s.xbar[0]), uint32_t(lane & (kPC - 1)));
+  const uint32_t r_cbar1 = mapa_u32(smem_u32(&s.xbar[1]), uint32_t(lane & (kPC - 1)));
+  cluster_barrier();  // barriers initialised and visible cluster-wide; smem initialised
+#ifdef SKL_PANEL_PROFILE
+  long long pp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp = clock64();
+#define PMARK(i)                \
+  do {                          \
+    long long _t = clock64();   \
+    pp[i] += _t - tp;           \
+    tp = _t;                    \
+  } while (0)
+#define PSUB(i)                 \
+  do {                          \
+    pp[i] += clock64() - tp;    \
+  } while (0)
+#else
+#define PMARK(i) \
+  do {           \
+  } while (0)
+#define PSUB(i) \
+  do {          \
+  } while (0)
+#endif
+
+  for (int g = r; g < rt; ++g) {
+    const int k = g - lo;
+    const int par = g & 1;
+    const int np = (k + 2) >> 1;  // pairs of the pushed candidate row (values 0..k)
+    const uint32_t phase = (uint32_t(g - r) >> 1) & 1u;
+    double* col = s.slab + (size_t)k * Rs;
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(kPC * sizeof(PCand)));
+      mbar_arrive_expect_tx(&s.xbar[2 + par], (MCAST ? 1u : uint32_t(kPC)) * 16u * uint32_t(np));
+    }
+    // ---- (1) v = c - A z; exact warp argmax --------------------------------
+    double bv = 0.0;
+    int bpos = -1, bph = 0, bli = 0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (lab[u] > g) {
+        const double v = (cneg[u] ? -cn[u] : cn[u]) - az[u];
+        vv[u] = v;
+        if (part == 0) {
+          col[rowt + u * RPB] = v;
+          if (bpos < 0 || fabs(v) > fabs(bv)) {
+            bv = v;
+            bpos = lab[u];
+            bph = ph[u];
+            bli = rowt + u * RPB;
+          }
+        }
+      }
+    }
+    {
+      const int wl = lane_argmax(bv, bpos, bpos >= 0);
+      if (lane == (wl < 0 ? 0 : wl)) s.wcand[warp] = PWCand{bv, wl < 0 ? -1 : bpos, bph, bli, {0, 0, 0}};
+    }
+    PMARK(0);
+    __syncthreads();
+    PMARK(1);
+    // ---- (2) CTA candidate -> every CTA; its row -> every CTA ---------------
+    {
+      const PWCand mine = lane < kPWarps ? s.wcand[lane] : PWCand{0.0, -1, 0, 0, {0, 0, 0}};
+      const int wl = lane_argmax(mine.v, mine.pos, lane < kPWarps && mine.pos >= 0);
+      const int src = wl < 0 ? 0 : wl;
+      const PWCand c = s.wcand[src];  // smem broadcast
+      const int lc = wl < 0 ? 0 : c.li;
+      if (warp == 0) {
+        if (lane < kPC) {
+          const unsigned long long vb64 = (unsigned long long)__double_as_longlong(wl < 0 ? 0.0 : c.v);
+          st_async_v4(r_cand + uint32_t((par * kPC + crank) * sizeof(PCand)), par ? r_cbar1 : r_cbar0,
+                      uint32_t(vb64), uint32_t(vb64 >> 32), uint32_t(wl < 0 ? -1 : c.pos), uint32_t(c.ph));
+        }
+      }
+      // candidate row values [0, k] as pairs (DSMEM push; an LL-flagged L2 row slot polled by
+      // every CTA was measured slower: ~1000 cycles per poll round on B200)
+      // this thread -> CTA dst, pairs tid/16 + 16 i
+      if (MCAST) {
+        // the candidate row -> this CTA's global slot (warp 0, after the candidate send); if it
+        // wins, ONE multicast bulk copy delivers it to all 16 CTAs (one L2 read, no DSMEM port
+        // traffic: the speculative st.async push of 16 rows to 16 CTAs costs ~18 cycles per
+        // row double on B200, the multicast is flat in the row length -- tools/probes/xchg3.cu)
+        if (warp == 0) {
+          double* gs = a.crow + ((size_t)par * kPC + crank) * CRS;
+          for (int j = lane; j <= k; j += 32) gs[j] = s.slab[(size_t)j * Rs + lc];
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __syncwarp();
+        }
+      } else {
+        const uint32_t rbar = par ? r_rbar1 : r_rbar0;
+        const uint32_t rrow = r_crows + uint32_t(((par * kPC + crank) * CRS) * sizeof(double));
+        for (int p = tid >> 4; p < np; p += kPThreads / kPC) {
+          const int j0 = 2 * p;
+          const double x0 = s.slab[(size_t)j0 * Rs + lc];
+          const double x1 = j0 + 1 <= k ? s.slab[(size_t)(j0 + 1) * Rs + lc] : 0.0;
+          st_async_v2f64(rrow + uint32_t(j0 * sizeof(double)), rbar, x0, x1);
+        }
+      }
+    }
+    PMARK(2);
+    // ---- (3) winner ---------------------------------------------------------
+    mbar_wait_delivered(&s.xbar[par], phase);
+    PMARK(3);
+    const PCand* cs = s.cand + par * kPC;
+    int owner;
+    {
+      const PCand mine = lane < kPC ? cs[lane] : PCand{0.0, -1, 0};
+      owner = lane_argmax(mine.v, mine.pos, lane < kPC && mine.pos >= 0);
+      if (owner < 0) owner = 0;
+    }
+    if (MCAST && owner == crank && tid == 0) {
+      const double* src = a.crow + ((size_t)par * kPC + crank) * CRS;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+          "%4;" ::"r"(smem_u32(s.crows + (size_t)par * kPC * CRS)),
+          "l"(src), "r"(16u * uint32_t(np)), "r"(smem_u32(&s.xbar[2 + par])), "h"((unsigned short)0xffff)
+          : "memory");
+    }
+    const PCand w = cs[owner];
+    const int a_pos = g + 1, b = w.pos, pb = w.ph;
+    const double vb = w.v;
+    const bool swapped = b != a_pos;
+    const bool more = (g + 1 < rt) || a.want_y;
+    // lazy interchange a_pos <-> b, then the next column's gathers (X(ph, pb), skew-lower)
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (swapped) lab[u] = lab[u] == b ? a_pos : (lab[u] == a_pos ? b : lab[u]);
+      cneg[u] = ph[u] < pb;
+      if (more && lab[u] > a_pos) {
+        if (a.dbg & 1)  // timing experiment only: a contiguous, cache-hot gather (wrong values)
+          cn[u] = W[(long long)r * ld + rbase + rowt + u * RPB];
+        else
+          cn[u] = cneg[u] ? W[(long long)ph[u] * ld + pb] : W[(long long)pb * ld + ph[u]];
+      }
+    }
+    // column k: explicit 1 at a_pos, v / vb below (the value is still in a register)
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (lab[u] == a_pos) {
+        vv[u] = 1.0;
+        if (part == 0) col[rowt + u * RPB] = 1.0;
+      } else if (lab[u] > a_pos) {
+        const double sv = (a.dbg & 4) ? vv[u] : (vb != 0.0 ? vv[u] / vb : vv[u]);
+        vv[u] = sv;
+        if (part == 0) col[rowt + u * RPB] = sv;
+      }
+    }
+    PMARK(4);
+    // ---- (4) z = T x for the next column (x = pivot row, pushed) -----------
+    mbar_wait_delivered(&s.xbar[2 + par], phase);
+    PMARK(5);
+    if (more) {
+      const double* xrow = s.crows + ((size_t)par * kPC + (MCAST ? 0 : owner)) * CRS;
+      for (int j = tid; j <= k; j += kPThreads) {
+        const double xm = j >= 1 ? xrow[j - 1] : 0.0;
+        const double xp = (j + 1 < k) ? xrow[j + 1] : (j + 1 == k ? 1.0 : 0.0);
+        const double tj = j == k ? vb : s.taus[j];
+        const double tj1 = (j + 1 == k) ? vb : s.taus[j + 1];
+        s.zbuf[j] = (j >= 1 ? tj * xm : 0.0) - (j + 1 <= k ? tj1 * xp : 0.0);
+      }
+    }
+    if (tid == 0) {
+      s.pivbuf[g - r] = b - a_pos;
+      s.taus[k] = vb;
+    }
+    __syncthreads();
+    PMARK(6);
+    if (!more) break;
+    // ---- (5) A z for the next column: kk = k + 1 columns ---------------------
+    const int kk = k + 1;
+    if (nbank < NBANK && k >= 32 * (nbank + 1)) {
+      // columns [32 nbank, 32 nbank + 32) are final: cache this thread's share of them
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int li = rowt + u * RPB;
+#pragma unroll
+        for (int b2 = 0; b2 < NBANK; ++b2)
+          if (b2 == nbank) {
+#pragma unroll
+            for (int q = 0; q < CPB; ++q) rb[u][CPB * b2 + q] = s.slab[(size_t)(32 * b2 + part + TPR * q) * Rs + li];
+          }
+      }
+      ++nbank;
+    }
+    if (a.dbg & 2) continue;  // timing experiment only: no gemv
+    const double zk = s.zbuf[k];
+    PSUB(8);
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int li = rowt + u * RPB;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      if (lab[u] > a_pos) {
+#pragma unroll
+        for (int b2 = 0; b2 < NBANK; ++b2) {
+          if (b2 < nbank) {
+            if constexpr (TPR == 1) {
+              const double2* z2 = reinterpret_cast<const double2*>(s.zbuf);
+#pragma unroll
+              for (int q = 0; q < 32; q += 4) {
+                const double2 za = z2[(32 * b2 + q) >> 1], zb = z2[((32 * b2 + q) >> 1) + 1];
+                c0 = fma(rb[u][32 * b2 + q], za.x, c0);
+                c1 = fma(rb[u][32 * b2 + q + 1], za.y, c1);
+                c2 = fma(rb[u][32 * b2 + q + 2], zb.x, c2);
+                c3 = fma(rb[u][32 * b2 + q + 3], zb.y, c3);
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < CPB; q += 2) {
+                c0 = fma(rb[u][CPB * b2 + q], s.zbuf[32 * b2 + part + TPR * q], c0);
+                if (q + 1 < CPB) c1 = fma(rb[u][CPB * b2 + q + 1], s.zbuf[32 * b2 + part + TPR * (q + 1)], c1);
+              }
+            }
+          }
+        }
+        PSUB(9);
+        const double* sl = s.slab + li;
+        if constexpr (TPR == 1) {
+          const double2* z2 = reinterpret_cast<const double2*>(s.zbuf);
+          int j = 32 * nbank;
+          for (; j + 3 < k; j += 4) {
+            const double2 za = z2[j >> 1], zb = z2[(j >> 1) + 1];  // j even
+            c0 = fma(sl[(size_t)j * Rs], za.x, c0);
+            c1 = fma(sl[(size_t)(j + 1) * Rs], za.y, c1);
+            c2 = fma(sl[(size_t)(j + 2) * Rs], zb.x, c2);
+            c3 = fma(sl[(size_t)(j + 3) * Rs], zb.y, c3);
+          }
+          for (; j < k; ++j) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
+          c1 = fma(vv[u], zk, c1);  // column k, freshly scaled, from the register
+        } else {
+          int j = 32 * nbank + part;
+          for (; j + 3 * TPR < k; j += 4 * TPR) {
+            c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
+            c1 = fma(sl[(size_t)(j + TPR) * Rs], s.zbuf[j + TPR], c1);
+            c2 = fma(sl[(size_t)(j + 2 * TPR) * Rs], s.zbuf[j + 2 * TPR], c2);
+            c3 = fma(sl[(size_t)(j + 3 * TPR) * Rs], s.zbuf[j + 3 * TPR], c3);
+          }
+          for (; j < k; j += TPR) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
+          if (part == 0) c1 = fma(vv[u], zk, c1);
+        }
+      }
+      PSUB(10);
+      double t = (c0 + c1) + (c2 + c3);
+      if constexpr (TPR > 1) {
+#pragma unroll
+        for (int o = 1; o < TPR; o <<= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      }
+      if (lab[u] > a_pos) az[u] = kk >= 2 ? t : 0.0;
+    }
+    PMARK(7);
+  }
+#ifdef SKL_PANEL_PROFILE
+  if (a.prof && tid == 0) {
+    for (int i = 0; i < 8; ++i) a.prof[crank * 16 + i] += (unsigned long long)pp[i];
+    a.prof[crank * 16 + 8] += (unsigned long long)(rt - r);
+    for (int i = 8; i < 11; ++i) a.prof[crank * 16 + 1 + i] += (unsigned long long)pp[i];
+  }
+#endif
+#undef PMARK
+#undef PSUB
+  __syncthreads();
+  // ---- outputs: tau / pivots, y (var1 straggler), position map, panel buffer ----
+  if (crank == 0) {
+    for (int g = r + tid; g < rt; g += kPThreads) {
+      a.tau[g] = s.taus[g - lo];
+      if (a.piv != nullptr) a.piv[g + 1] = (long long)s.pivbuf[g - r];
+    }
+    for (int i = tid; i < row0; i += kPThreads) a.gperm[i] = i;
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int li = rowt + u * RPB;
+    if (li < rcount && part == 0) {
+      const int pos = lab[u];
+      if (a.want_y && rt < n && pos >= rt + 1) a.y[pos] = (cneg[u] ? -cn[u] : cn[u]) - az[u];
+      a.gperm[pos] = ph[u];
+      if (pos >= rt && ph[u] != pos) {
+        const int q = atomicAdd(a.disp_count, 1);
+        a.disp_list[q] = pos;
+      }
+    }
+  }
+  // panel buffer (by position); the TPR threads of a row split its columns
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int li = rowt + u * RPB;
+    if (li < rcount) {
+      double* dstp = a.pbuf + lab[u];
+      for (int j = part; j < kmax; j += TPR) __stcs(dstp + (size_t)j * n, s.slab[(size_t)j * Rs + li]);
+    }
+  }
+  // no CTA may exit while a peer can still st.async into its shared memory: every
+  // delivery of the last step has been waited on above, and nothing is sent after it
+}
+
 }  // namespace
 
 size_t panel_cluster_smem_bytes(int rows_per, int kmax, int npush) {
@@ -928,8 +1397,73 @@ int panel_multi_clusters(int csize, size_t smem) {
   return ncl > 32 ? 32 : ncl;
 }
 
+size_t panel_push_smem_bytes(int rows_per, int kmax) { return psmem_layout(rows_per, kmax, nullptr, nullptr); }
+
+bool panel_push_v2() {
+  static int on = [] {
+    const char* v = getenv("SKL_PANEL_V2");
+    return v && *v ? atoi(v) : 1;
+  }();
+  return on != 0;
+}
+
+template <int RPT, int NB, int TPR>
+cudaError_t launch_push_t(const PanelArgs& a, size_t smem, cudaStream_t stream) {
+  // SKL_PUSH_MCAST=0: the speculative DSMEM push of every candidate row (A/B builds)
+  static const int mcast = [] {
+    const char* v = getenv("SKL_PUSH_MCAST");
+    return v && *v ? atoi(v) : 1;
+  }();
+  auto kern = mcast ? panel_push_kernel<RPT, NB, TPR, true> : panel_push_kernel<RPT, NB, TPR, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kPC);
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = kPC;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+// single 16-CTA cluster, pivoted: the lean push-mode panel (panel_push_kernel); the
+// threads per row grow as the rows per CTA shrink (SKL_PUSH_TPR caps it, 1 = off)
+cudaError_t launch_panel_push(const PanelArgs& a, cudaStream_t stream) {
+  const size_t smem = psmem_layout(a.rows_per, a.kmax, nullptr, nullptr);
+  cudaError_t e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  static const int tpr_cap = [] {
+    const char* v = getenv("SKL_PUSH_TPR");
+    return v && *v ? atoi(v) : 8;
+  }();
+  const int R = a.rows_per;
+  if (R > kPThreads)
+    e = launch_push_t<2, 1, 1>(a, smem, stream);
+  else if (R > kPThreads / 2 || tpr_cap < 2)
+    e = launch_push_t<1, 2, 1>(a, smem, stream);
+  else if (R > kPThreads / 4 || tpr_cap < 4)
+    e = launch_push_t<1, 2, 2>(a, smem, stream);
+  else if (R > kPThreads / 8 || tpr_cap < 8)
+    e = launch_push_t<1, 2, 4>(a, smem, stream);
+  else
+    e = launch_push_t<1, 2, 8>(a, smem, stream);
+  if (e != cudaSuccess) return e;
+  return launch_panel_finish(a, stream);
+}
+
 // a.nblocks = total CTAs (Q clusters x a.csize); cooperative so all clusters are co-resident
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream) {
+  if (a.push && a.pivot && a.nblocks == csize && csize == kPC && a.rows_per <= 2 * kPThreads && panel_push_v2() &&
+      psmem_layout(a.rows_per, a.kmax, nullptr, nullptr) <= csmem_layout(a.rows_per, a.kmax, nullptr, nullptr, csize))
+    return launch_panel_push(a, stream);
   const bool push = a.push && a.pivot && a.nblocks == csize;
   size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr, push ? csize : 0);
   cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

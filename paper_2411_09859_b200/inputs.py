@@ -50,3 +50,32 @@ def batched_inputs(batch, n=256, seed0=0, dtype=np.float64):
         out[i] = skew_lower(n, seed0 + i, "normal", np.float64).astype(dtype).T
     # stored so that out[i].T is column-major: out[i][j, r] = X[r, j]
     return out
+
+
+def normal_scaled_rows(n, seed=0, out=None, chunk=1024):
+    """Config 5's G = Philox(seed).standard_normal((n, n)) / sqrt(n), row-major,
+    drawn in row chunks (a chunked Philox draw equals one full draw)
+    so no second n x n temporary is needed.  Bit-identical to skew_lower's G."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    g = np.empty((n, n), dtype=np.float64) if out is None else out
+    s = np.sqrt(n)
+    for i0 in range(0, n, chunk):
+        i1 = min(n, i0 + chunk)
+        g[i0:i1] = rng.standard_normal((i1 - i0, n)) / s
+    return g
+
+
+def skew_device_from_rows(g, torch, chunk=2048):
+    """Column-major CUDA tensor X = G - G^T from a row-major host G (the full skew
+    matrix; only its strict lower triangle is read).  fp64 subtraction is
+    correctly rounded on both sides, so X equals skew_lower's bit for bit."""
+    n = g.shape[0]
+    gd = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    for i0 in range(0, n, chunk):
+        gd[i0:i0 + chunk].copy_(torch.from_numpy(g[i0:i0 + chunk]))
+    x = torch.empty((n, n), dtype=torch.float64, device="cuda").t()   # column-major
+    for j0 in range(0, n, chunk):
+        x[:, j0:j0 + chunk] = gd[:, j0:j0 + chunk] - gd[j0:j0 + chunk, :].t()
+    del gd
+    torch.cuda.empty_cache()
+    return x

@@ -55,18 +55,27 @@ def test_config4_f64_golden(golden):
 
 
 def test_config4_f32_golden(golden):
-    """fp32: pivots/log|Pf| vs the reference's own fp32 run.  Rounding-level
-    near-ties can flip an fp32 pivot in any implementation, so a small number
-    of matrices may take a different (equally valid) pivot path; the Pfaffian
-    magnitude must still agree to fp32 accuracy for all of them."""
+    """fp32 (config 4) against the reference's own fp32 run (the pfaffian path,
+    apps.py:12-30 -> ltlt_blk_piv(b=256) in float32): bit-exact pivot sequences
+    for all 128 fixture matrices, identical Pfaffian signs for all 8192, and
+    log|Pf| within the north star's fp32 tolerance (1e-3 relative).  On a pivot
+    flip the message names the matrix, the step and the top-2 margin of that
+    step (measured in fp64 on the same fp32 matrix) so the flip can be judged."""
     g = golden("cfg4_batch_f32.npz")
     xs = np.stack([skew_lower(256, i).astype(np.float32) for i in range(8192)])
     L, tau, piv, sign, logabs = apps().ltlt_batched_piv(xs)
-    same = np.array([np.array_equal(piv[i], g["piv"][i]) for i in range(128)])
-    assert same.mean() >= 0.95
-    assert np.mean(sign == g["sign"]) >= 0.99
+    flips = [i for i in range(128) if not np.array_equal(piv[i], g["piv"][i])]
+    if flips:
+        i = flips[0]
+        k = int(np.flatnonzero(piv[i] != g["piv"][i])[0])
+        marg = oracle.pivot_margins(xs[i].astype(np.float64), b=256)
+        pytest.fail(f"fp32 pivots differ in {len(flips)}/128 matrices; first: matrix {i} step {k} "
+                    f"(gpu {piv[i][k]} vs reference {g['piv'][i][k]}), fp64 top-2 margin at step {k - 1}: "
+                    f"{marg[k - 1]:.3e}")
+    assert np.array_equal(sign, g["sign"])
     rel = np.abs(logabs - g["logpf"]) / np.abs(g["logpf"])
     assert np.median(rel) <= 1e-5 and np.max(rel) <= 1e-3
+    assert np.allclose(tau[:128], g["tau"], rtol=1e-3, atol=1e-3 * np.abs(g["tau"]).max())
 
 
 @pytest.mark.parametrize("n", [257, 300, 512])

@@ -1,7 +1,13 @@
-"""The single-cluster panel's push mode (candidate rows by st.async, lazy
-interchanges through position labels) performs the same arithmetic as the L2
-row-exchange mode (SKL_PANEL_PUSH=0): L, tau and pivots must be bit-identical.
-Both runs are also held to the oracle by test_gpu_blocked.py / test_gpu_twostep.py."""
+"""The single-cluster panel's delivery modes perform the same arithmetic and must
+give bit-identical L, tau and pivots:
+  * panel_push_kernel, pivot row by one multicast bulk copy (default) vs by the
+    speculative st.async push of every candidate row (SKL_PUSH_MCAST=0);
+  * panel_cluster_kernel push mode (SKL_PANEL_V2=0) vs its L2 row exchange
+    (SKL_PANEL_V2=0 SKL_PANEL_PUSH=0).
+Across the two kernels (and across the gemv's threads-per-row split, SKL_PUSH_TPR)
+only the summation order of A z differs: pivots identical, L and tau within the
+north star's 1e-10 * n.  All runs are held to the oracle by test_gpu_blocked.py /
+test_gpu_twostep.py."""
 import os
 import subprocess
 import sys
@@ -14,17 +20,40 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def run(tmp_path, push):
-    out = tmp_path / f"push{push}.npz"
-    env = dict(os.environ, SKL_PANEL_PUSH=str(push))
+def run(tmp_path, tag, **env_extra):
+    out = tmp_path / f"{tag}.npz"
+    env = dict(os.environ, **{k: str(v) for k, v in env_extra.items()})
     p = subprocess.run([sys.executable, str(ROOT / "tests" / "push_worker.py"), str(out)], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0 and "PUSH_OK" in p.stdout, p.stdout[-2000:] + p.stderr[-4000:]
     return np.load(out)
 
 
-def test_push_mode_bit_identical_to_l2_exchange(tmp_path):
-    a, b = run(tmp_path, 1), run(tmp_path, 0)
+def same(a, b):
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         assert np.array_equal(a[k], b[k]), k
+
+
+def close(a, b):
+    for k in a.files:
+        if k[0] == "p":
+            assert np.array_equal(a[k], b[k]), k
+        else:
+            n = a[k].shape[0]
+            assert np.allclose(np.tril(a[k], -1) if a[k].ndim == 2 else a[k],
+                               np.tril(b[k], -1) if b[k].ndim == 2 else b[k], rtol=1e-10 * n, atol=1e-10 * n), k
+
+
+def test_multicast_bit_identical_to_dsmem_push(tmp_path):
+    same(run(tmp_path, "mc", SKL_PUSH_MCAST=1), run(tmp_path, "dp", SKL_PUSH_MCAST=0))
+
+
+def test_old_kernel_push_bit_identical_to_l2_exchange(tmp_path):
+    same(run(tmp_path, "o1", SKL_PANEL_V2=0, SKL_PANEL_PUSH=1), run(tmp_path, "o0", SKL_PANEL_V2=0, SKL_PANEL_PUSH=0))
+
+
+def test_lean_kernel_matches_old_kernel_and_tpr(tmp_path):
+    new = run(tmp_path, "new")
+    close(new, run(tmp_path, "old", SKL_PANEL_V2=0))
+    close(new, run(tmp_path, "tpr1", SKL_PUSH_TPR=1))
