@@ -145,7 +145,13 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       static int min_w = env_int("SKL_MIN_CLUSTER_W", 64);
       static int ll_single = env_int("SKL_LL_SINGLE", 1);
       const int npush = (ll_single && panel_push()) ? C : 0;  // room for the pushed candidate rows
-      int w = (gpu_nb > 0 && want > gpu_nb) ? gpu_nb : want;
+      // tall panels (more than SKL_GPU_NB_ROWS rows) use SKL_GPU_NB_TALL columns: the lean
+      // panel kernel register-caches 64 slab columns of a 256-row CTA, wider tall panels
+      // stream the rest from shared memory every step
+      static int nb_tall = env_int("SKL_GPU_NB_TALL", 0);
+      static int tall_rows = env_int("SKL_GPU_NB_ROWS", 2048);
+      const int cap = (nb_tall > 0 && rows > tall_rows) ? nb_tall : gpu_nb;
+      int w = (cap > 0 && want > cap) ? cap : want;
       while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo, npush) > smem_limit()) --w;
       if (w >= 1 && w >= std::min(want, min_w)) {
         // default (SKL_LL_SINGLE=1): the one cluster runs the multi-cluster kernel with

@@ -979,6 +979,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   const int rcount = max(0, min(R, n - rbase));
   const int rt = r + nelim;
   const int CRS = push_crs(kmax);
+#ifdef SKL_PANEL_DBG_BUILD
+  const int dbg = a.dbg;  // timing experiments only (make variant VFLAGS=-DSKL_PANEL_DBG_BUILD)
+#else
+  constexpr int dbg = 0;
+#endif
   PSmem s;
   psmem_layout(R, kmax, &s, smem_raw);
 
@@ -1047,7 +1052,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     double* col = s.slab + (size_t)k * Rs;
     if (tid == 0) {
       mbar_arrive_expect_tx(&s.xbar[par], uint32_t(kPC * sizeof(PCand)));
-      mbar_arrive_expect_tx(&s.xbar[2 + par], (MCAST ? 1u : uint32_t(kPC)) * 16u * uint32_t(np));
+      if (!(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], (MCAST ? 1u : uint32_t(kPC)) * 16u * uint32_t(np));
     }
     // ---- (1) v = c - A z; exact warp argmax --------------------------------
     double bv = 0.0;
@@ -1092,7 +1097,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       // candidate row values [0, k] as pairs (DSMEM push; an LL-flagged L2 row slot polled by
       // every CTA was measured slower: ~1000 cycles per poll round on B200)
       // this thread -> CTA dst, pairs tid/16 + 16 i
-      if (MCAST) {
+      if (dbg & 8) {
+      } else if (MCAST) {
         // the candidate row -> this CTA's global slot (warp 0, after the candidate send); if it
         // wins, ONE multicast bulk copy delivers it to all 16 CTAs (one L2 read, no DSMEM port
         // traffic: the speculative st.async push of 16 rows to 16 CTAs costs ~18 cycles per
@@ -1125,7 +1131,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       owner = lane_argmax(mine.v, mine.pos, lane < kPC && mine.pos >= 0);
       if (owner < 0) owner = 0;
     }
-    if (MCAST && owner == crank && tid == 0) {
+    if (MCAST && owner == crank && tid == 0 && !(dbg & 8)) {
       const double* src = a.crow + ((size_t)par * kPC + crank) * CRS;
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
@@ -1143,8 +1149,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     for (int u = 0; u < RPT; ++u) {
       if (swapped) lab[u] = lab[u] == b ? a_pos : (lab[u] == a_pos ? b : lab[u]);
       cneg[u] = ph[u] < pb;
-      if (more && lab[u] > a_pos) {
-        if (a.dbg & 1)  // timing experiment only: a contiguous, cache-hot gather (wrong values)
+      if (more && lab[u] > a_pos && !(dbg & 16)) {
+        if (dbg & 1)  // timing experiment only: a contiguous, cache-hot gather (wrong values)
           cn[u] = W[(long long)r * ld + rbase + rowt + u * RPB];
         else
           cn[u] = cneg[u] ? W[(long long)ph[u] * ld + pb] : W[(long long)pb * ld + ph[u]];
@@ -1157,14 +1163,14 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
         vv[u] = 1.0;
         if (part == 0) col[rowt + u * RPB] = 1.0;
       } else if (lab[u] > a_pos) {
-        const double sv = (a.dbg & 4) ? vv[u] : (vb != 0.0 ? vv[u] / vb : vv[u]);
+        const double sv = (dbg & 4) ? vv[u] : (vb != 0.0 ? vv[u] / vb : vv[u]);
         vv[u] = sv;
         if (part == 0) col[rowt + u * RPB] = sv;
       }
     }
     PMARK(4);
     // ---- (4) z = T x for the next column (x = pivot row, pushed) -----------
-    mbar_wait_delivered(&s.xbar[2 + par], phase);
+    if (!(dbg & 8)) mbar_wait_delivered(&s.xbar[2 + par], phase);
     PMARK(5);
     if (more) {
       const double* xrow = s.crows + ((size_t)par * kPC + (MCAST ? 0 : owner)) * CRS;
@@ -1199,7 +1205,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       }
       ++nbank;
     }
-    if (a.dbg & 2) continue;  // timing experiment only: no gemv
+    if (dbg & 2) continue;  // timing experiment only: no gemv
     const double zk = s.zbuf[k];
     PSUB(8);
 #pragma unroll
