@@ -150,9 +150,18 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       // stream the rest from shared memory every step
       static int nb_tall = env_int("SKL_GPU_NB_TALL", 0);
       static int tall_rows = env_int("SKL_GPU_NB_ROWS", 2048);
-      const int cap = (nb_tall > 0 && rows > tall_rows) ? nb_tall : gpu_nb;
+      // short trailing matrices: ONE panel finishes them (no trailing GEMMs left) when the
+      // whole slab fits the lean panel kernel's shared memory (SKL_FINAL_ROWS)
+      static int final_rows = env_int("SKL_FINAL_ROWS", 600);
+      int cap = (nb_tall > 0 && rows > tall_rows) ? nb_tall : gpu_nb;
+      if (rows <= final_rows) cap = want;
       int w = (cap > 0 && want > cap) ? cap : want;
-      while (w >= 1 && skl::panel_cluster_smem_bytes(Rc, r + w - lo, npush) > smem_limit()) --w;
+      auto fits = [&](int ww) {
+        const int km = r + ww - lo;
+        if (ll_single && skl::panel_push_usable(panel_push(), C, C, Rc, km)) return true;
+        return skl::panel_cluster_smem_bytes(Rc, km, npush) <= smem_limit();
+      };
+      while (w >= 1 && !fits(w)) --w;
       if (w >= 1 && w >= std::min(want, min_w)) {
         // default (SKL_LL_SINGLE=1): the one cluster runs the multi-cluster kernel with
         // Q = 1 -- st.async candidate all-to-all + flagged pivot rows through L2, no
@@ -932,6 +941,8 @@ int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int r
       a.prof = nullptr;
       a.pivot = 1;
       a.info = nullptr;
+      // the same panel kernel as the single-device driver (bit-identical factorizations)
+      a.push = (p.cluster == 2 && p.ctas == p.csize && panel_push()) ? 1 : 0;
       KScope ks(KPANEL, st);
       if (p.cluster == 2)
         SKL_TRY(skl::launch_panel_multi(a, p.csize, st));
