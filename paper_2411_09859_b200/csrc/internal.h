@@ -124,6 +124,9 @@ cudaError_t launch_panel(const PanelArgs& a, cudaStream_t stream);
 // single-cluster variant (DSMEM exchange); cluster size 16 (or 8), 0 if unavailable
 int panel_cluster_size();
 size_t panel_cluster_smem_bytes(int rows_per, int kmax, int npush = 0);
+// the lean single-cluster push panel (panel_push_kernel): shared memory, and whether a plan runs on it
+size_t panel_push_smem_bytes(int rows_per, int kmax);
+bool panel_push_usable(bool push_pivot, int ctas, int csize, int rows_per, int kmax);
 cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
 // multi-cluster variant (cooperative; intra-cluster DSMEM + inter-cluster LL exchange)
 int panel_multi_clusters(int csize, size_t smem);

@@ -891,7 +891,8 @@ struct PSmem {
   uint64_t* xbar; // [4]: candidates (par), rows (2 + par)
 };
 
-__host__ __device__ inline size_t psmem_layout(int R, int kmax, PSmem* s, unsigned char* base) {
+// nslots: pivot-row slots per parity (1 with the multicast delivery, 16 with the DSMEM push)
+__host__ __device__ inline size_t psmem_layout(int R, int kmax, PSmem* s, unsigned char* base, int nslots = 1) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -902,7 +903,7 @@ __host__ __device__ inline size_t psmem_layout(int R, int kmax, PSmem* s, unsign
   unsigned char* p;
   p = take(sizeof(double) * (size_t)kmax * Rs);
   if (s) s->slab = (double*)p;
-  p = take(sizeof(double) * 2 * kPC * (size_t)push_crs(kmax));
+  p = take(sizeof(double) * 2 * nslots * (size_t)push_crs(kmax));
   if (s) s->crows = (double*)p;
   p = take(sizeof(double) * (kmax + 2));
   if (s) s->zbuf = (double*)p;
@@ -967,6 +968,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   constexpr int CPB = 32 / TPR;          // cached columns per bank and thread
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int crank = int(cg::this_cluster().block_rank());
+  const int C = int(cg::this_cluster().num_blocks());  // <= 16
+  constexpr int NSLOT = MCAST ? 1 : kPC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int part = TPR > 1 ? (tid & (TPR - 1)) : 0;
   const int rowt = TPR > 1 ? tid / TPR : tid;  // this thread's (first) local row
@@ -985,7 +988,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   constexpr int dbg = 0;
 #endif
   PSmem s;
-  psmem_layout(R, kmax, &s, smem_raw);
+  psmem_layout(R, kmax, &s, smem_raw, NSLOT);
 
   if (tid == 0) {
     for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);
@@ -1014,13 +1017,15 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   double rb[RPT][CPB * NBANK];
   int nbank = 0;
   // remote addresses, fixed for the whole panel
-  const uint32_t dst = uint32_t(tid & (kPC - 1));
-  const uint32_t r_crows = mapa_u32(smem_u32(s.crows), dst);
-  const uint32_t r_rbar0 = mapa_u32(smem_u32(&s.xbar[2]), dst);
-  const uint32_t r_rbar1 = mapa_u32(smem_u32(&s.xbar[3]), dst);
-  const uint32_t r_cand = mapa_u32(smem_u32(s.cand), uint32_t(lane & (kPC - 1)));
-  const uint32_t r_cbar0 = mapa_u32(smem_u32(&s.xbar[0]), uint32_t(lane & (kPC - 1)));
-  const uint32_t r_cbar1 = mapa_u32(smem_u32(&s.xbar[1]), uint32_t(lane & (kPC - 1)));
+  const uint32_t dst = uint32_t(tid & (kPC - 1));  // DSMEM push: this thread's destination CTA (if < C)
+  const uint32_t dstc = dst < uint32_t(C) ? dst : 0u;
+  const uint32_t r_crows = mapa_u32(smem_u32(s.crows), dstc);
+  const uint32_t r_rbar0 = mapa_u32(smem_u32(&s.xbar[2]), dstc);
+  const uint32_t r_rbar1 = mapa_u32(smem_u32(&s.xbar[3]), dstc);
+  const uint32_t lanec = uint32_t(lane < C ? lane : 0);
+  const uint32_t r_cand = mapa_u32(smem_u32(s.cand), lanec);
+  const uint32_t r_cbar0 = mapa_u32(smem_u32(&s.xbar[0]), lanec);
+  const uint32_t r_cbar1 = mapa_u32(smem_u32(&s.xbar[1]), lanec);
   cluster_barrier();  // barriers initialised and visible cluster-wide; smem initialised
 #ifdef SKL_PANEL_PROFILE
   long long pp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -1051,8 +1056,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     const uint32_t phase = (uint32_t(g - r) >> 1) & 1u;
     double* col = s.slab + (size_t)k * Rs;
     if (tid == 0) {
-      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(kPC * sizeof(PCand)));
-      if (!(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], (MCAST ? 1u : uint32_t(kPC)) * 16u * uint32_t(np));
+      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C * sizeof(PCand)));
+      if (!(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], (MCAST ? 1u : uint32_t(C)) * 16u * uint32_t(np));
     }
     // ---- (1) v = c - A z; exact warp argmax --------------------------------
     double bv = 0.0;
@@ -1088,7 +1093,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       const PWCand c = s.wcand[src];  // smem broadcast
       const int lc = wl < 0 ? 0 : c.li;
       if (warp == 0) {
-        if (lane < kPC) {
+        if (lane < C) {
           const unsigned long long vb64 = (unsigned long long)__double_as_longlong(wl < 0 ? 0.0 : c.v);
           st_async_v4(r_cand + uint32_t((par * kPC + crank) * sizeof(PCand)), par ? r_cbar1 : r_cbar0,
                       uint32_t(vb64), uint32_t(vb64 >> 32), uint32_t(wl < 0 ? -1 : c.pos), uint32_t(c.ph));
@@ -1104,7 +1109,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
         // traffic: the speculative st.async push of 16 rows to 16 CTAs costs ~18 cycles per
         // row double on B200, the multicast is flat in the row length -- tools/probes/xchg3.cu)
         if (warp == 0) {
-          double* gs = a.crow + ((size_t)par * kPC + crank) * CRS;
+          double* gs = a.crow + ((size_t)par * kPC + crank) * CRS;  // global slots: [2][16][CRS]
           for (int j = lane; j <= k; j += 32) gs[j] = s.slab[(size_t)j * Rs + lc];
           asm volatile("fence.proxy.async.global;" ::: "memory");
           __syncwarp();
@@ -1112,7 +1117,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       } else {
         const uint32_t rbar = par ? r_rbar1 : r_rbar0;
         const uint32_t rrow = r_crows + uint32_t(((par * kPC + crank) * CRS) * sizeof(double));
-        for (int p = tid >> 4; p < np; p += kPThreads / kPC) {
+        for (int p = tid >> 4; dst < uint32_t(C) && p < np; p += kPThreads / kPC) {
           const int j0 = 2 * p;
           const double x0 = s.slab[(size_t)j0 * Rs + lc];
           const double x1 = j0 + 1 <= k ? s.slab[(size_t)(j0 + 1) * Rs + lc] : 0.0;
@@ -1127,16 +1132,16 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     const PCand* cs = s.cand + par * kPC;
     int owner;
     {
-      const PCand mine = lane < kPC ? cs[lane] : PCand{0.0, -1, 0};
-      owner = lane_argmax(mine.v, mine.pos, lane < kPC && mine.pos >= 0);
+      const PCand mine = lane < C ? cs[lane] : PCand{0.0, -1, 0};
+      owner = lane_argmax(mine.v, mine.pos, lane < C && mine.pos >= 0);
       if (owner < 0) owner = 0;
     }
     if (MCAST && owner == crank && tid == 0 && !(dbg & 8)) {
       const double* src = a.crow + ((size_t)par * kPC + crank) * CRS;
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
-          "%4;" ::"r"(smem_u32(s.crows + (size_t)par * kPC * CRS)),
-          "l"(src), "r"(16u * uint32_t(np)), "r"(smem_u32(&s.xbar[2 + par])), "h"((unsigned short)0xffff)
+          "%4;" ::"r"(smem_u32(s.crows + (size_t)par * CRS)),
+          "l"(src), "r"(16u * uint32_t(np)), "r"(smem_u32(&s.xbar[2 + par])), "h"((unsigned short)((1u << C) - 1u))
           : "memory");
     }
     const PCand w = cs[owner];
@@ -1173,7 +1178,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     if (!(dbg & 8)) mbar_wait_delivered(&s.xbar[2 + par], phase);
     PMARK(5);
     if (more) {
-      const double* xrow = s.crows + ((size_t)par * kPC + (MCAST ? 0 : owner)) * CRS;
+      const double* xrow = s.crows + ((size_t)par * NSLOT + (MCAST ? 0 : owner)) * CRS;
       for (int j = tid; j <= k; j += kPThreads) {
         const double xm = j >= 1 ? xrow[j - 1] : 0.0;
         const double xp = (j + 1 < k) ? xrow[j + 1] : (j + 1 == k ? 1.0 : 0.0);
@@ -1403,7 +1408,23 @@ int panel_multi_clusters(int csize, size_t smem) {
   return ncl > 32 ? 32 : ncl;
 }
 
-size_t panel_push_smem_bytes(int rows_per, int kmax) { return psmem_layout(rows_per, kmax, nullptr, nullptr); }
+int push_mcast();
+size_t panel_push_smem_bytes(int rows_per, int kmax) {
+  return psmem_layout(rows_per, kmax, nullptr, nullptr, push_mcast() ? 1 : kPC);
+}
+
+bool panel_push_v2();
+bool panel_push_usable(bool push_pivot, int ctas, int csize, int rows_per, int kmax) {
+  static int lim = 0;
+  if (!lim) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&lim, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || lim <= 0)
+      lim = 232448;
+  }
+  return push_pivot && ctas == csize && csize >= 1 && csize <= kPC && rows_per <= 2 * kPThreads && panel_push_v2() &&
+         panel_push_smem_bytes(rows_per, kmax) <= (size_t)lim;
+}
 
 bool panel_push_v2() {
   static int on = [] {
@@ -1413,26 +1434,30 @@ bool panel_push_v2() {
   return on != 0;
 }
 
-template <int RPT, int NB, int TPR>
-cudaError_t launch_push_t(const PanelArgs& a, size_t smem, cudaStream_t stream) {
-  // SKL_PUSH_MCAST=0: the speculative DSMEM push of every candidate row (A/B builds)
+// SKL_PUSH_MCAST=0: the speculative DSMEM push of every candidate row (A/B builds)
+int push_mcast() {
   static const int mcast = [] {
     const char* v = getenv("SKL_PUSH_MCAST");
     return v && *v ? atoi(v) : 1;
   }();
-  auto kern = mcast ? panel_push_kernel<RPT, NB, TPR, true> : panel_push_kernel<RPT, NB, TPR, false>;
+  return mcast;
+}
+
+template <int RPT, int NB, int TPR>
+cudaError_t launch_push_t(const PanelArgs& a, size_t smem, cudaStream_t stream) {
+  auto kern = push_mcast() ? panel_push_kernel<RPT, NB, TPR, true> : panel_push_kernel<RPT, NB, TPR, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kPC);
+  cfg.gridDim = dim3(a.nblocks);
   cfg.blockDim = dim3(kPThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = kPC;
+  attr.val.clusterDim.x = a.nblocks;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
@@ -1443,7 +1468,7 @@ cudaError_t launch_push_t(const PanelArgs& a, size_t smem, cudaStream_t stream) 
 // single 16-CTA cluster, pivoted: the lean push-mode panel (panel_push_kernel); the
 // threads per row grow as the rows per CTA shrink (SKL_PUSH_TPR caps it, 1 = off)
 cudaError_t launch_panel_push(const PanelArgs& a, cudaStream_t stream) {
-  const size_t smem = psmem_layout(a.rows_per, a.kmax, nullptr, nullptr);
+  const size_t smem = panel_push_smem_bytes(a.rows_per, a.kmax);
   cudaError_t e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   static const int tpr_cap = [] {
@@ -1467,9 +1492,7 @@ cudaError_t launch_panel_push(const PanelArgs& a, cudaStream_t stream) {
 
 // a.nblocks = total CTAs (Q clusters x a.csize); cooperative so all clusters are co-resident
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream) {
-  if (a.push && a.pivot && a.nblocks == csize && csize == kPC && a.rows_per <= 2 * kPThreads && panel_push_v2() &&
-      psmem_layout(a.rows_per, a.kmax, nullptr, nullptr) <= csmem_layout(a.rows_per, a.kmax, nullptr, nullptr, csize))
-    return launch_panel_push(a, stream);
+  if (panel_push_usable(a.push && a.pivot, a.nblocks, csize, a.rows_per, a.kmax)) return launch_panel_push(a, stream);
   const bool push = a.push && a.pivot && a.nblocks == csize;
   size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr, push ? csize : 0);
   cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
