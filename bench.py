@@ -412,10 +412,10 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def panel_dram_traffic(path=Path(__file__).resolve().parent / "profiles" / "r01_panel_dram_n4096_v10.csv"):
+def panel_dram_traffic(path=Path(__file__).resolve().parent / "profiles" / "r02_panel_dram_n4096.csv"):
     """Mean DRAM bytes (read + write) per panel_cluster_kernel launch of one config-2
     factorization, from the committed ncu capture (``ncu --metrics dram__bytes_read.sum,
-    dram__bytes_write.sum -k regex:panel_cluster python tools/run_blk.py --reps 1``; the
+    dram__bytes_write.sum -k regex:panel_push python tools/run_blk.py --reps 1``; the
     second factorization's launches).  None when the capture is absent."""
     import csv
     if not path.exists():
@@ -550,7 +550,7 @@ def main():
         per_launch_bytes = alg_bytes / cnt["panel"]
         per_launch_s = per_fact["panel"] / cnt["panel"] * 1e-3
         ach = per_launch_bytes / per_launch_s / 1e9
-        roof = {"kernel": "panel_cluster_kernel (pivoted left-looking panel)", "bound": "hbm",
+        roof = {"kernel": "panel_push_kernel (pivoted left-looking panel, one 16-CTA cluster)", "bound": "hbm",
                 "achieved": round(ach, 2), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                 "traffic": panel_dram_traffic(), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": int(per_launch_bytes), "launches_per_step": cnt["panel"]}

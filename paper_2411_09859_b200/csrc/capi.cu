@@ -152,7 +152,7 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       static int tall_rows = env_int("SKL_GPU_NB_ROWS", 2048);
       // short trailing matrices: ONE panel finishes them (no trailing GEMMs left) when the
       // whole slab fits the lean panel kernel's shared memory (SKL_FINAL_ROWS)
-      static int final_rows = env_int("SKL_FINAL_ROWS", 600);
+      static int final_rows = env_int("SKL_FINAL_ROWS", 0);  // measured slower at 600 (config 1: 1.025 -> 1.076 ms)
       int cap = (nb_tall > 0 && rows > tall_rows) ? nb_tall : gpu_nb;
       if (rows <= final_rows) cap = want;
       int w = (cap > 0 && want > cap) ? cap : want;

@@ -990,9 +990,18 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   PSmem s;
   psmem_layout(R, kmax, &s, smem_raw, NSLOT);
 
-  if (tid == 0) {
+  // the deliveries of step g complete on xbar[g & 1] (candidates) and xbar[2 + (g & 1)]
+  // (pivot row); the last thread arms each barrier for step g + 2 as soon as step g's
+  // wait returns, so no arming sits on warp 0's path to the candidate send
+  constexpr int kArm = kPThreads - 1;
+  auto row_bytes = [&](int gg) { return (MCAST ? 1u : uint32_t(C)) * 16u * uint32_t((gg - lo + 2) >> 1); };
+  if (tid == kArm) {
     for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);
     fence_mbar_init();
+    for (int gg = r; gg < rt && gg < r + 2; ++gg) {
+      mbar_arrive_expect_tx(&s.xbar[gg & 1], uint32_t(C * sizeof(PCand)));
+      mbar_arrive_expect_tx(&s.xbar[2 + (gg & 1)], row_bytes(gg));
+    }
   }
   for (int j = tid; j < kmax + 2; j += kPThreads) {
     s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
@@ -1028,7 +1037,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   const uint32_t r_cbar1 = mapa_u32(smem_u32(&s.xbar[1]), lanec);
   cluster_barrier();  // barriers initialised and visible cluster-wide; smem initialised
 #ifdef SKL_PANEL_PROFILE
-  long long pp[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long pp[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   long long tp = clock64();
 #define PMARK(i)                \
   do {                          \
@@ -1055,10 +1064,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     const int np = (k + 2) >> 1;  // pairs of the pushed candidate row (values 0..k)
     const uint32_t phase = (uint32_t(g - r) >> 1) & 1u;
     double* col = s.slab + (size_t)k * Rs;
-    if (tid == 0) {
-      mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C * sizeof(PCand)));
-      if (!(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], (MCAST ? 1u : uint32_t(C)) * 16u * uint32_t(np));
-    }
+    PSUB(11);
     // ---- (1) v = c - A z; exact warp argmax --------------------------------
     double bv = 0.0;
     int bpos = -1, bph = 0, bli = 0;
@@ -1078,6 +1084,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
         }
       }
     }
+    PSUB(12);  // v computed (gathered value consumed)
     {
       const int wl = lane_argmax(bv, bpos, bpos >= 0);
       if (lane == (wl < 0 ? 0 : wl)) s.wcand[warp] = PWCand{bv, wl < 0 ? -1 : bpos, bph, bli, {0, 0, 0}};
@@ -1128,6 +1135,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     PMARK(2);
     // ---- (3) winner ---------------------------------------------------------
     mbar_wait_delivered(&s.xbar[par], phase);
+    if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C * sizeof(PCand)));
     PMARK(3);
     const PCand* cs = s.cand + par * kPC;
     int owner;
@@ -1176,6 +1184,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     PMARK(4);
     // ---- (4) z = T x for the next column (x = pivot row, pushed) -----------
     if (!(dbg & 8)) mbar_wait_delivered(&s.xbar[2 + par], phase);
+    if (tid == kArm && g + 2 < rt && !(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], row_bytes(g + 2));
     PMARK(5);
     if (more) {
       const double* xrow = s.crows + ((size_t)par * NSLOT + (MCAST ? 0 : owner)) * CRS;
@@ -1255,14 +1264,21 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
           for (; j < k; ++j) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
           c1 = fma(vv[u], zk, c1);  // column k, freshly scaled, from the register
         } else {
-          int j = 32 * nbank + part;
-          for (; j + 3 * TPR < k; j += 4 * TPR) {
-            c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
-            c1 = fma(sl[(size_t)(j + TPR) * Rs], s.zbuf[j + TPR], c1);
-            c2 = fma(sl[(size_t)(j + 2 * TPR) * Rs], s.zbuf[j + 2 * TPR], c2);
-            c3 = fma(sl[(size_t)(j + 3 * TPR) * Rs], s.zbuf[j + 3 * TPR], c3);
+          // four predicated column loads per trip, all issued before the FMAs (a short
+          // dependent LDS -> FMA chain: with TPR threads per row a thread has few columns)
+          for (int j = 32 * nbank + part; j < k; j += 4 * TPR) {
+            double x[4], zz[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int jj = j + e * TPR;
+              x[e] = jj < k ? sl[(size_t)jj * Rs] : 0.0;
+              zz[e] = jj < k ? s.zbuf[jj] : 0.0;
+            }
+            c0 = fma(x[0], zz[0], c0);
+            c1 = fma(x[1], zz[1], c1);
+            c2 = fma(x[2], zz[2], c2);
+            c3 = fma(x[3], zz[3], c3);
           }
-          for (; j < k; j += TPR) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
           if (part == 0) c1 = fma(vv[u], zk, c1);
         }
       }
@@ -1280,7 +1296,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   if (a.prof && tid == 0) {
     for (int i = 0; i < 8; ++i) a.prof[crank * 16 + i] += (unsigned long long)pp[i];
     a.prof[crank * 16 + 8] += (unsigned long long)(rt - r);
-    for (int i = 8; i < 11; ++i) a.prof[crank * 16 + 1 + i] += (unsigned long long)pp[i];
+    for (int i = 8; i < 13; ++i) a.prof[crank * 16 + 1 + i] += (unsigned long long)pp[i];
   }
 #endif
 #undef PMARK

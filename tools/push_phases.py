@@ -30,4 +30,5 @@ for case in sys.argv[1:]:
         st = max(p[c, 8], 1)
         print(json.dumps({"n": n, "w": w, "cta": c, "steps": int(st), "sum": round(p[c, :8].sum() / st),
                           **{NAMES[i]: round(p[c, i] / st) for i in range(8)},
-                          "gemv_sub(zk,cached,uncached)": [round(p[c, 9 + i] / st) for i in range(3)]}))
+                          "gemv_sub(zk,cached,uncached)": [round(p[c, 9 + i] / st) for i in range(3)],
+                          "p1_sub(armed,v_done)": [round(p[c, 12 + i] / st) for i in range(2)]}))
