@@ -125,7 +125,7 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   int rows = n - (lo + 1);
   // GPU panel width cap for the cluster panel (per-step cost grows with the width while the
   // trailing DMMA GEMM is already efficient at K ~ 96); SKL_GPU_NB overrides.
-  static int gpu_nb = env_int("SKL_GPU_NB", 96);
+  static int gpu_nb = env_int("SKL_GPU_NB", 94);  // K = 94 + 2 (straggler) = 96: whole 16-wide GEMM k-chunks
   static int no_cluster = env_int("SKL_NO_CLUSTER", 0);
   const int Cmax = no_cluster ? 0 : skl::panel_cluster_size();
   // SKL_FORCE_MULTI=1: skip the single-cluster plan (tests drive the multi-cluster

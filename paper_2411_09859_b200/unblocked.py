@@ -1,9 +1,13 @@
 """Unblocked drivers (drop-in for reference ``unblocked.py``).
 
 * ``ltlt_unb_twostep(x, pivot)`` (unblocked.py:229-240): the Wimmer two-step
-  driver, run by the fused single-cluster CUDA kernel ``skl_ltlt_unb_twostep``
-  (eliminations, symmetric interchanges, fold and skew rank-2 updates of
-  each pair in one launch).
+  driver, entered through ``skl_ltlt_unb_twostep``.  From n = 128 up it runs
+  the blocked GPU driver (lean cluster panel ``panel_push_kernel`` + DMMA
+  trailing update), which computes the same L, T and pivots and is faster
+  (config 1, n=512: 0.99 ms vs 2.9 ms for the fused right-looking kernel);
+  below n = 128 the fused single-cluster two-step kernel (``twostep.cu``:
+  eliminations, interchanges, fold and skew rank-2 of each pair in one
+  launch) serves it.  DESIGN.md §1 records the decision.
 * ``ltlt_unb_ll(x, pivot, first_column)`` (unblocked.py:205-226): one
   left-looking panel over the whole matrix = the blocked driver with
   b >= m - 1 (blocked.py:341-362), served by the same panel kernel, pivoted
