@@ -16,6 +16,7 @@
 // narrows the panel when it would not fit (the factorization is invariant to
 // the GPU block width; pivots stay those of the reference).
 #include <cooperative_groups.h>
+#include <cassert>
 
 #include "common.cuh"
 #include "internal.h"
@@ -1007,6 +1008,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
     s.zbuf[j] = 0.0;
   }
+#ifdef SKL_CHECKED
+  assert(C >= 1 && C <= kPC && R <= RPT * RPB && kmax <= n && lo >= -1 && r >= lo && rt <= n - 1 + 1);
+  assert(psmem_layout(R, kmax, nullptr, nullptr, MCAST ? 1 : kPC) <= 232448);
+#endif
   // per-row state in registers: row li = rowt + u * RPB
   int lab[RPT], ph[RPT];
   double cn[RPT], az[RPT], vv[RPT];
@@ -1155,6 +1160,14 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     const PCand w = cs[owner];
     const int a_pos = g + 1, b = w.pos, pb = w.ph;
     const double vb = w.v;
+#ifdef SKL_CHECKED
+    // checked build (make variant V=checked VFLAGS=-DSKL_CHECKED): the invariants the
+    // exchange relies on -- a real winner below g, inside the panel's rows, identical
+    // in every CTA (each CTA re-derives it from the same delivered candidates)
+    assert(owner >= 0 && owner < C);
+    assert(b >= a_pos && b < n && pb >= row0 && pb < n);
+    assert(w.pos == cs[owner].pos);
+#endif
     const bool swapped = b != a_pos;
     const bool more = (g + 1 < rt) || a.want_y;
     // lazy interchange a_pos <-> b, then the next column's gathers (X(ph, pb), skew-lower)
@@ -1165,8 +1178,22 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       if (more && lab[u] > a_pos && !(dbg & 16)) {
         if (dbg & 1)  // timing experiment only: a contiguous, cache-hot gather (wrong values)
           cn[u] = W[(long long)r * ld + rbase + rowt + u * RPB];
+        else if (dbg & 64)  // timing experiment only: every gather from column pb (mirrored-storage proxy)
+          cn[u] = W[(long long)pb * ld + ph[u]];
         else
           cn[u] = cneg[u] ? W[(long long)ph[u] * ld + pb] : W[(long long)pb * ld + ph[u]];
+        if (dbg & 32) {
+          // remote-gather proxy: the gathered value additionally waits on a chain of
+          // (dbg >> 8) dependent L2 loads (peer-memory latency stand-in, timing only)
+          long long idx = (long long)pb * ld + ph[u];
+          double acc = 0.0;
+          for (int h = 0; h < (dbg >> 8); ++h) {
+            const double t = __ldcg(W + (idx & ((1ll << 20) - 1)));  // within the first 8 MB of W
+            acc += t * 0.0;
+            idx += 1 + (long long)(t != t);
+          }
+          cn[u] += acc;
+        }
       }
     }
     // column k: explicit 1 at a_pos, v / vb below (the value is still in a register)
@@ -1315,6 +1342,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     const int li = rowt + u * RPB;
     if (li < rcount && part == 0) {
       const int pos = lab[u];
+#ifdef SKL_CHECKED
+      assert(pos >= row0 && pos < n && ph[u] >= row0 && ph[u] < n);
+#endif
       if (a.want_y && rt < n && pos >= rt + 1) a.y[pos] = (cneg[u] ? -cn[u] : cn[u]) - az[u];
       a.gperm[pos] = ph[u];
       if (pos >= rt && ph[u] != pos) {
