@@ -19,6 +19,7 @@
 // mask i <= j at load and store, so the upper triangle is never read or
 // written (test_core.py:39-58 NaN-poison invariant).
 #include <algorithm>
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -341,6 +342,104 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
   bulk_wait0();
 }
 
+// Small trailing updates (few 128x128 tiles: the late panels of config 2, config 1):
+// one CTA of 4 warps per 64x64 lower tile, several CTAs per SM.  A 64-row tile is
+// one half (m8 blocks 0-7 or 8-15) of a packed 128-row tile, i.e. a contiguous 2 KiB
+// piece of every 4 KiB k4 block, streamed by bulk copies through a 3-stage ring.
+// Each C element accumulates the same DMMA k4 blocks in the same order as in
+// gemm_lower_nt_kernel and is added to C once, so the result is bit-identical.
+constexpr int kSmT = 64, kSmThreads = 128, kSmStages = 3, kSmK4 = 4;
+constexpr int kSmHalf = 8 * 32;  // doubles of a half k4 block (8 m8 blocks)
+constexpr size_t kSmSmem = size_t(kSmStages) * 2 * kSmK4 * kSmHalf * sizeof(double) + 2 * kSmStages * 8 + 128;
+
+__global__ void __launch_bounds__(kSmThreads) gemm_lower_small_kernel(const double* __restrict__ P,
+                                                                      const double* __restrict__ Q, int k4cap,
+                                                                      int nk4, double* __restrict__ C, long long ldc,
+                                                                      int n, double beta) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sP = reinterpret_cast<double*>(smem_raw);
+  double* sQ = sP + kSmStages * kSmK4 * kSmHalf;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + kSmStages * kSmK4 * kSmHalf);
+  const int t = blockIdx.x;
+  int ti = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  const int tj = t - ti * (ti + 1) / 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int nch = (nk4 + kSmK4 - 1) / kSmK4;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < kSmStages; ++s2) mbar_init(&full[s2], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // half k4 block q of 64-tile x: packed 128-tile x/2, m8 blocks (x&1)*8 .. +7
+  auto issue = [&](int c) {
+    const int s2 = c % kSmStages;
+    const int q0 = c * kSmK4, nb = min(kSmK4, nk4 - q0);
+    mbar_arrive_expect_tx(&full[s2], uint32_t(2 * nb * kSmHalf * sizeof(double)));
+    for (int q = 0; q < nb; ++q) {
+      const double* ps = P + (((size_t)(ti >> 1) * k4cap + q0 + q) * 16 + (ti & 1) * 8) * 32;
+      const double* qs = Q + (((size_t)(tj >> 1) * k4cap + q0 + q) * 16 + (tj & 1) * 8) * 32;
+      bulk_g2s(sP + ((size_t)s2 * kSmK4 + q) * kSmHalf, ps, kSmHalf * sizeof(double), &full[s2]);
+      bulk_g2s(sQ + ((size_t)s2 * kSmK4 + q) * kSmHalf, qs, kSmHalf * sizeof(double), &full[s2]);
+    }
+  };
+  if (tid == 0)
+    for (int c = 0; c < min(kSmStages, nch); ++c) issue(c);
+  // this thread's C entries, loaded now so their latency hides behind the k loop
+  const int row_base = ti * kSmT + wm * 32 + (lane >> 2);
+  const int col_base = tj * kSmT + wn * 32 + 2 * (lane & 3);
+  double cin[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = row_base + mi * 8, col = col_base + ni * 8 + e;
+        cin[mi][ni][e] = (beta != 0.0 && row < n && col < n && row > col) ? C[(long long)col * ldc + row] : 0.0;
+      }
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    const int s2 = c % kSmStages;
+    mbar_wait(&full[s2], (c / kSmStages) & 1);
+    const int nb = min(kSmK4, nk4 - c * kSmK4);
+    const double* ps = sP + (size_t)s2 * kSmK4 * kSmHalf + (wm * 4) * 32 + lane;
+    const double* qs = sQ + (size_t)s2 * kSmK4 * kSmHalf + (wn * 4) * 32 + lane;
+    for (int kb = 0; kb < nb; ++kb) {
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = ps[kb * kSmHalf + mi * 32];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = qs[kb * kSmHalf + ni * 32];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+    __syncthreads();  // stage s2 consumed by every warp
+    if (tid == 0 && c + kSmStages < nch) {
+      fence_proxy_async();
+      issue(c + kSmStages);
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int row = row_base + mi * 8, col = col_base + ni * 8 + e;
+        if (row < n && col < n && row > col)
+          C[(long long)col * ldc + row] = (beta == 1.0 ? cin[mi][ni][e] : beta * cin[mi][ni][e]) + acc[mi][ni][e];
+      }
+}
+
 __device__ __forceinline__ void packed_decode(size_t off, int k4cap, int& row, int& col) {
   int lane = int(off & 31);
   int mb = int((off >> 5) & 15);
@@ -590,6 +689,24 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   int nt = tiles_for(n);
   int ntiles = own ? own->ntiles : nt * (nt + 1) / 2;
   if (ntiles == 0) return cudaSuccess;
+  // few 128x128 tiles (under two waves): 64x64 tiles, one 4-warp CTA each (bit-identical)
+  static const int small_max = [] {
+    const char* v = getenv("SKL_GEMM_SMALL_TILES");
+    return v && *v ? atoi(v) : 2 * 148;
+  }();
+  if (!own && tri && ncols == n && nk4_dev == nullptr && ntiles < small_max) {
+    static bool sattr = false;
+    if (!sattr) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_lower_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)kSmSmem);
+      if (e != cudaSuccess) return e;
+      sattr = true;
+    }
+    const int nt64 = (n + kSmT - 1) / kSmT;
+    gemm_lower_small_kernel<<<nt64 * (nt64 + 1) / 2, kSmThreads, kSmSmem, stream>>>(P, Q, k4cap, nk4, C, ldc, n,
+                                                                                   beta);
+    return cudaGetLastError();
+  }
   int grid = ntiles < nsm ? ntiles : nsm;
   if (own)
     gemm_lower_nt_kernel<true><<<grid, kGemmThreads, kGemmSmem, stream>>>(

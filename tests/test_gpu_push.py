@@ -60,3 +60,9 @@ def test_lean_kernel_matches_old_kernel_and_tpr(tmp_path):
     new = run(tmp_path, "new")
     close(new, run(tmp_path, "old", SKL_PANEL_V2=0))
     close(new, run(tmp_path, "tpr1", SKL_PUSH_TPR=1))
+
+
+def test_small_tile_gemm_bit_identical(tmp_path):
+    # trailing updates with few 128x128 tiles run on 64x64-tile CTAs (gemm_lower_small_kernel):
+    # same DMMA k order per element, one add into C -> bit-identical factors
+    same(run(tmp_path, "small", SKL_GEMM_SMALL_TILES=296), run(tmp_path, "big", SKL_GEMM_SMALL_TILES=0))
