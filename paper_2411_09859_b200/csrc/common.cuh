@@ -38,6 +38,21 @@ __device__ __forceinline__ void ll_get2(const uint64_t* p, uint32_t flag, uint32
   d1 = uint32_t(w1);
 }
 
+// two flagged pairs (a 4-word record) polled together: one L2 round trip per attempt
+__device__ __forceinline__ void ll_get4(const uint64_t* p, uint32_t flag, uint32_t& d0, uint32_t& d1, uint32_t& d2,
+                                        uint32_t& d3) {
+  uint64_t w0, w1, w2, w3;
+  do {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w2), "=l"(w3) : "l"(p + 2) : "memory");
+  } while (uint32_t(w0 >> 32) != flag || uint32_t(w1 >> 32) != flag || uint32_t(w2 >> 32) != flag ||
+           uint32_t(w3 >> 32) != flag);
+  d0 = uint32_t(w0);
+  d1 = uint32_t(w1);
+  d2 = uint32_t(w2);
+  d3 = uint32_t(w3);
+}
+
 // three flagged pairs (a 6-word record) polled together: one L2 round trip per
 // attempt instead of three dependent ones
 __device__ __forceinline__ void ll_get6(const uint64_t* p, uint32_t flag, uint32_t& d0, uint32_t& d1, uint32_t& d2,

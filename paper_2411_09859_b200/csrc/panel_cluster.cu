@@ -1366,6 +1366,344 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   // delivery of the last step has been waited on above, and nothing is sent after it
 }
 
+
+// ===========================================================================
+// panel_multi2_kernel: the pivoted panel on Q co-resident clusters of C CTAs
+// (tall panels of configs 3 and 5), on the lean structure of panel_push_kernel.
+// Per step: the intra-cluster exchange is panel_push_kernel's (candidates by
+// st.async, every CTA re-derives its cluster's winner); the CTA holding a
+// cluster's winner publishes ONE record {v, position, physical row} and the
+// winner's row [0, k] as LL-flagged words (value + step tag, no fence needed)
+// into its cluster's L2 slot; warp 0 of every CTA polls the Q records (one lane
+// each) and picks the global winner; every thread j <= k polls the two words of
+// the winning row that z_j needs.  Two L2 round trips per step (record, row)
+// instead of the leader relay + separate pivot-row and row-a exchanges of
+// panel_cluster_kernel<MULTI>.
+// ===========================================================================
+template <int RPT, int NBANK>
+__global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = int(cluster.num_blocks());
+  const int crank = int(cluster.block_rank());
+  const int gcta = blockIdx.x;
+  const int Q = int(gridDim.x) / C;
+  const int qid = gcta / C;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n, lo = a.lo, r = a.r, nelim = a.nelim, kmax = a.kmax;
+  const int R = a.rows_per, Rs = cslab_stride(R);
+  const long long ld = a.ld;
+  const double* __restrict__ W = a.W;
+  const int row0 = lo + 1;
+  const int rbase = row0 + gcta * R;
+  const int rcount = max(0, min(R, n - rbase));
+  const int rt = r + nelim;
+  PSmem s;
+  psmem_layout(R, kmax, &s, smem_raw, 3);
+  // the winning cluster's L2 slot (record: 3 flagged pairs; row: k+1 flagged doubles)
+  // lands here by one multicast bulk copy issued by the cluster leader, per parity
+  const int SW = 6 + 2 * (kmax + 1);
+  uint64_t* mslot = reinterpret_cast<uint64_t*>(s.crows);
+  constexpr int kArm = kPThreads - 1;
+  auto slot_bytes = [&](int gg) { return uint32_t(sizeof(uint64_t)) * uint32_t(6 + 2 * (gg - lo + 1)); };
+  if (tid == kArm) {
+    for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);
+    fence_mbar_init();
+    for (int gg = r; gg < rt && gg < r + 2; ++gg) {
+      mbar_arrive_expect_tx(&s.xbar[gg & 1], uint32_t(C * sizeof(PCand)));
+      mbar_arrive_expect_tx(&s.xbar[2 + (gg & 1)], slot_bytes(gg));
+    }
+  }
+  for (int j = tid; j < kmax + 2; j += kPThreads) {
+    s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
+    s.zbuf[j] = 0.0;
+  }
+  int lab[RPT], ph[RPT];
+  double cn[RPT], az[RPT], vv[RPT];
+  bool cneg[RPT];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int li = tid + u * kPThreads;
+    const int pos = rbase + li;
+    lab[u] = li < rcount ? pos : -1;
+    ph[u] = pos;
+    az[u] = 0.0;
+    vv[u] = 0.0;
+    cneg[u] = false;
+    cn[u] = (li < rcount && pos > r) ? W[(long long)r * ld + pos] : 0.0;
+    if (li < rcount && lo < r) s.slab[li] = W[(long long)lo * ld + pos];
+  }
+  double rb[RPT][32 * NBANK];
+  int nbank = 0;
+  const uint32_t lanec = uint32_t(lane < C ? lane : 0);
+  const uint32_t r_cand = mapa_u32(smem_u32(s.cand), lanec);
+  const uint32_t r_cbar0 = mapa_u32(smem_u32(&s.xbar[0]), lanec);
+  const uint32_t r_cbar1 = mapa_u32(smem_u32(&s.xbar[1]), lanec);
+  cluster_barrier();
+#ifdef SKL_PANEL_PROFILE
+  long long pp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tp = clock64();
+#define QMARK(i)              \
+  do {                        \
+    long long _t = clock64(); \
+    pp[i] += _t - tp;         \
+    tp = _t;                  \
+  } while (0)
+#else
+#define QMARK(i) \
+  do {           \
+  } while (0)
+#endif
+
+  for (int g = r; g < rt; ++g) {
+    const int k = g - lo;
+    const int par = g & 1;
+    const uint32_t phase = (uint32_t(g - r) >> 1) & 1u;
+    const uint32_t tag = a.tag0 + uint32_t(g - r);
+    double* col = s.slab + (size_t)k * Rs;
+    // ---- (1) v = c - A z; exact warp argmax --------------------------------
+    double bv = 0.0;
+    int bpos = -1, bph = 0, bli = 0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (lab[u] > g) {
+        const double v = (cneg[u] ? -cn[u] : cn[u]) - az[u];
+        vv[u] = v;
+        col[tid + u * kPThreads] = v;
+        if (bpos < 0 || fabs(v) > fabs(bv)) {
+          bv = v;
+          bpos = lab[u];
+          bph = ph[u];
+          bli = tid + u * kPThreads;
+        }
+      }
+    }
+    {
+      const int wl = lane_argmax(bv, bpos, bpos >= 0);
+      if (lane == (wl < 0 ? 0 : wl)) s.wcand[warp] = PWCand{bv, wl < 0 ? -1 : bpos, bph, bli, {0, 0, 0}};
+    }
+    __syncthreads();
+    QMARK(0);
+    // ---- (2) CTA candidate -> every CTA of the cluster ------------------------
+    int lc;
+    {
+      const PWCand mine = lane < kPWarps ? s.wcand[lane] : PWCand{0.0, -1, 0, 0, {0, 0, 0}};
+      const int wl = lane_argmax(mine.v, mine.pos, lane < kPWarps && mine.pos >= 0);
+      const PWCand c = s.wcand[wl < 0 ? 0 : wl];
+      lc = wl < 0 ? 0 : c.li;
+      if (warp == 0 && lane < C) {
+        const unsigned long long vb64 = (unsigned long long)__double_as_longlong(wl < 0 ? 0.0 : c.v);
+        st_async_v4(r_cand + uint32_t((par * kPC + crank) * sizeof(PCand)), par ? r_cbar1 : r_cbar0,
+                    uint32_t(vb64), uint32_t(vb64 >> 32), uint32_t(wl < 0 ? -1 : c.pos), uint32_t(c.ph));
+      }
+    }
+    QMARK(1);
+    // ---- (3) cluster winner; its CTA publishes record + row to the cluster's L2 slot
+    mbar_wait_delivered(&s.xbar[par], phase);
+    QMARK(2);
+    if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C * sizeof(PCand)));
+    {
+      const PCand* cs = s.cand + par * kPC;
+      const PCand mine = lane < C ? cs[lane] : PCand{0.0, -1, 0};
+      int cown = lane_argmax(mine.v, mine.pos, lane < C && mine.pos >= 0);
+      if (cown < 0) cown = 0;
+      if (cown == crank) {
+        const PCand cw = cs[cown];
+        uint64_t* slot = a.slots + ((size_t)qid * 2 + par) * a.slot_words;
+        if (tid == 0) {
+          const unsigned long long vb64 = (unsigned long long)__double_as_longlong(cw.v);
+          ll_put2(slot, uint32_t(vb64), uint32_t(vb64 >> 32), tag);
+          ll_put2(slot + 2, uint32_t(cw.pos), uint32_t(cw.ph), tag);
+          ll_put2(slot + 4, uint32_t(qid), 0u, tag);
+        }
+        for (int j = tid; j <= k; j += kPThreads) ll_put_double(slot + 6 + 2 * j, s.slab[(size_t)j * Rs + lc], tag);
+      }
+    }
+    QMARK(3);
+    // ---- (4) global winner: the cluster leader's warp 0 polls the Q records (one lane
+    // each) and multicasts the winning cluster's slot -- record and row -- into every
+    // CTA of its cluster; the copy is checked against the step tag (L2 fallback) ------
+    if (crank == 0 && warp == 0) {
+      PCand rec{0.0, -1, 0};
+      if (lane < Q) {
+        const uint64_t* slot = a.slots + ((size_t)lane * 2 + par) * a.slot_words;
+        uint32_t vlo, vhi, pp, pph;
+        ll_get4(slot, tag, vlo, vhi, pp, pph);  // both flagged pairs in one poll round
+        rec = PCand{__longlong_as_double((long long)((uint64_t(vhi) << 32) | vlo)), int(pp), int(pph)};
+      }
+      const int gl = lane_argmax(rec.v, rec.pos, lane < Q && rec.pos >= 0);
+      if (lane == 0) {
+        const uint64_t* src = a.slots + ((size_t)(gl < 0 ? 0 : gl) * 2 + par) * a.slot_words;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
+            "[%3], %4;" ::"r"(smem_u32(mslot + (size_t)par * SW)),
+            "l"(src), "r"(slot_bytes(g)), "r"(smem_u32(&s.xbar[2 + par])), "h"((unsigned short)((1u << C) - 1u))
+            : "memory");
+      }
+    }
+    QMARK(3);
+    mbar_wait_delivered(&s.xbar[2 + par], phase);
+    if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[2 + par], slot_bytes(g + 2));
+    const uint64_t* ms = mslot + (size_t)par * SW;
+    PCand w;
+    int wq;
+    {
+      uint64_t w0 = ms[0], w1 = ms[1], w2 = ms[2], w3 = ms[3], w4 = ms[4];
+      if (uint32_t(w0 >> 32) != tag || uint32_t(w1 >> 32) != tag || uint32_t(w2 >> 32) != tag ||
+          uint32_t(w3 >> 32) != tag || uint32_t(w4 >> 32) != tag) {
+        // the copy raced the publication (never seen): read the record through L2; the
+        // winning cluster is the one whose record the leader saw, i.e. any valid best
+        PCand best{0.0, -1, 0};
+        int bq = 0;
+        for (int q = 0; q < Q; ++q) {
+          const uint64_t* slot = a.slots + ((size_t)q * 2 + par) * a.slot_words;
+          uint32_t vlo, vhi, pp, pph;
+          ll_get4(slot, tag, vlo, vhi, pp, pph);
+          const PCand c{__longlong_as_double((long long)((uint64_t(vhi) << 32) | vlo)), int(pp), int(pph)};
+          if (c.pos >= 0 && (best.pos < 0 || fabs(c.v) > fabs(best.v) || (fabs(c.v) == fabs(best.v) && c.pos < best.pos))) {
+            best = c;
+            bq = q;
+          }
+        }
+        w = best;
+        wq = bq;
+      } else {
+        w = PCand{__longlong_as_double((long long)((uint64_t(uint32_t(w1)) << 32) | uint32_t(w0))), int(uint32_t(w2)),
+                  int(uint32_t(w3))};
+        wq = int(uint32_t(w4));
+      }
+    }
+    QMARK(4);
+    const int a_pos = g + 1, b = w.pos, pb = w.ph;
+    const double vb = w.v;
+    const bool swapped = b != a_pos;
+    const bool more = (g + 1 < rt) || a.want_y;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (swapped) lab[u] = lab[u] == b ? a_pos : (lab[u] == a_pos ? b : lab[u]);
+      cneg[u] = ph[u] < pb;
+      if (more && lab[u] > a_pos) cn[u] = cneg[u] ? W[(long long)ph[u] * ld + pb] : W[(long long)pb * ld + ph[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      if (lab[u] == a_pos) {
+        vv[u] = 1.0;
+        col[tid + u * kPThreads] = 1.0;
+      } else if (lab[u] > a_pos) {
+        const double sv = vb != 0.0 ? vv[u] / vb : vv[u];
+        vv[u] = sv;
+        col[tid + u * kPThreads] = sv;
+      }
+    }
+    QMARK(5);
+    // ---- (5) z = T x (x = the winning row, from the multicast copy) ----------------
+    if (more) {
+      const uint64_t* xs = ms + 6;
+      const uint64_t* xr = a.slots + ((size_t)wq * 2 + par) * a.slot_words + 6;
+      auto xval = [&](int j) {
+        const uint64_t lo = xs[2 * j], hi = xs[2 * j + 1];
+        if (uint32_t(lo >> 32) == tag && uint32_t(hi >> 32) == tag)
+          return __longlong_as_double((long long)((uint64_t(uint32_t(hi)) << 32) | uint32_t(lo)));
+        return ll_get_double(xr + 2 * j, tag);  // fallback through L2 (never seen)
+      };
+      for (int j = tid; j <= k; j += kPThreads) {
+        const double xm = j >= 1 ? xval(j - 1) : 0.0;
+        const double xp = (j + 1 < k) ? xval(j + 1) : (j + 1 == k ? 1.0 : 0.0);
+        const double tj = j == k ? vb : s.taus[j];
+        const double tj1 = (j + 1 == k) ? vb : s.taus[j + 1];
+        s.zbuf[j] = (j >= 1 ? tj * xm : 0.0) - (j + 1 <= k ? tj1 * xp : 0.0);
+      }
+    }
+    if (tid == 0) {
+      s.pivbuf[g - r] = b - a_pos;
+      s.taus[k] = vb;
+    }
+    __syncthreads();
+    QMARK(6);
+    if (!more) break;
+    // ---- (6) A z for the next column ---------------------------------------------
+    const int kk = k + 1;
+    if (nbank < NBANK && k >= 32 * (nbank + 1)) {
+#pragma unroll
+      for (int u = 0; u < RPT; ++u) {
+        const int li = tid + u * kPThreads;
+#pragma unroll
+        for (int b2 = 0; b2 < NBANK; ++b2)
+          if (b2 == nbank) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) rb[u][32 * b2 + q] = s.slab[(size_t)(32 * b2 + q) * Rs + li];
+          }
+      }
+      ++nbank;
+    }
+    const double2* z2 = reinterpret_cast<const double2*>(s.zbuf);
+    const double zk = s.zbuf[k];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+      const int li = tid + u * kPThreads;
+      if (lab[u] > a_pos) {
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+#pragma unroll
+        for (int b2 = 0; b2 < NBANK; ++b2) {
+          if (b2 < nbank) {
+#pragma unroll
+            for (int q = 0; q < 32; q += 4) {
+              const double2 za = z2[(32 * b2 + q) >> 1], zb = z2[((32 * b2 + q) >> 1) + 1];
+              c0 = fma(rb[u][32 * b2 + q], za.x, c0);
+              c1 = fma(rb[u][32 * b2 + q + 1], za.y, c1);
+              c2 = fma(rb[u][32 * b2 + q + 2], zb.x, c2);
+              c3 = fma(rb[u][32 * b2 + q + 3], zb.y, c3);
+            }
+          }
+        }
+        const double* sl = s.slab + li;
+        int j = 32 * nbank;
+        for (; j + 3 < k; j += 4) {
+          const double2 za = z2[j >> 1], zb = z2[(j >> 1) + 1];
+          c0 = fma(sl[(size_t)j * Rs], za.x, c0);
+          c1 = fma(sl[(size_t)(j + 1) * Rs], za.y, c1);
+          c2 = fma(sl[(size_t)(j + 2) * Rs], zb.x, c2);
+          c3 = fma(sl[(size_t)(j + 3) * Rs], zb.y, c3);
+        }
+        for (; j < k; ++j) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
+        c1 = fma(vv[u], zk, c1);
+        az[u] = kk >= 2 ? (c0 + c1) + (c2 + c3) : 0.0;
+      }
+    }
+    QMARK(7);
+  }
+#ifdef SKL_PANEL_PROFILE
+  if (a.prof && tid == 0 && gcta < 160) {
+    for (int i = 0; i < 8; ++i) a.prof[gcta * 16 + i] += (unsigned long long)pp[i];
+    a.prof[gcta * 16 + 8] += (unsigned long long)(rt - r);
+  }
+#endif
+#undef QMARK
+  __syncthreads();
+  if (gcta == 0) {
+    for (int g = r + tid; g < rt; g += kPThreads) {
+      a.tau[g] = s.taus[g - lo];
+      if (a.piv != nullptr) a.piv[g + 1] = (long long)s.pivbuf[g - r];
+    }
+    for (int i = tid; i < row0; i += kPThreads) a.gperm[i] = i;
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int li = tid + u * kPThreads;
+    if (li < rcount) {
+      const int pos = lab[u];
+      if (a.want_y && rt < n && pos >= rt + 1) a.y[pos] = (cneg[u] ? -cn[u] : cn[u]) - az[u];
+      a.gperm[pos] = ph[u];
+      if (pos >= rt && ph[u] != pos) {
+        const int q = atomicAdd(a.disp_count, 1);
+        a.disp_list[q] = pos;
+      }
+      double* dstp = a.pbuf + pos;
+      for (int j = 0; j < kmax; ++j) __stcs(dstp + (size_t)j * n, s.slab[(size_t)j * Rs + li]);
+    }
+  }
+}
+
 }  // namespace
 
 size_t panel_cluster_smem_bytes(int rows_per, int kmax, int npush) {
@@ -1536,9 +1874,60 @@ cudaError_t launch_panel_push(const PanelArgs& a, cudaStream_t stream) {
   return launch_panel_finish(a, stream);
 }
 
+size_t panel_multi2_smem_bytes(int rows_per, int kmax) { return psmem_layout(rows_per, kmax, nullptr, nullptr, 3); }
+
+// several co-resident clusters, pivoted: panel_multi2_kernel (SKL_PANEL_MULTI2=0 keeps the
+// round-1 panel_cluster_kernel<MULTI>)
+bool panel_multi2_usable(const PanelArgs& a, int csize) {
+  static const int on = [] {
+    const char* v = getenv("SKL_PANEL_MULTI2");
+    return v && *v ? atoi(v) : 1;
+  }();
+  if (!on || !a.pivot || csize < 1 || csize > kPC || a.nblocks % csize != 0 || a.nblocks / csize > 32 ||
+      a.rows_per > 2 * kPThreads || a.slot_words < 6 + 2 * (a.kmax + 1) ||
+      6 * push_crs(a.kmax) < 2 * (6 + 2 * (a.kmax + 1)))
+    return false;
+  return panel_multi2_smem_bytes(a.rows_per, a.kmax) <= 232448;
+}
+
+template <int RPT, int NB>
+cudaError_t launch_multi2_t(const PanelArgs& a, int csize, size_t smem, cudaStream_t stream) {
+  auto kern = panel_multi2_kernel<RPT, NB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.nblocks);
+  cfg.blockDim = dim3(kPThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = csize;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeCooperative;
+  attrs[1].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+cudaError_t launch_panel_multi2(const PanelArgs& a, int csize, cudaStream_t stream) {
+  const size_t smem = panel_multi2_smem_bytes(a.rows_per, a.kmax);
+  cudaError_t e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  e = a.rows_per > kPThreads ? launch_multi2_t<2, 1>(a, csize, smem, stream)
+                             : launch_multi2_t<1, 2>(a, csize, smem, stream);
+  if (e != cudaSuccess) return e;
+  return launch_panel_finish(a, stream);
+}
+
 // a.nblocks = total CTAs (Q clusters x a.csize); cooperative so all clusters are co-resident
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream) {
   if (panel_push_usable(a.push && a.pivot, a.nblocks, csize, a.rows_per, a.kmax)) return launch_panel_push(a, stream);
+  if (a.nblocks > csize && panel_multi2_usable(a, csize)) return launch_panel_multi2(a, csize, stream);
   const bool push = a.push && a.pivot && a.nblocks == csize;
   size_t smem = csmem_layout(a.rows_per, a.kmax, nullptr, nullptr, push ? csize : 0);
   cudaError_t e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

@@ -5,8 +5,12 @@ sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_2411_09859_b200 import _capi, device as dv
 from paper_2411_09859_b200.inputs import skew_lower
+import os
 NAMES = ["v+warp_argmax", "sync1", "cta_cand+push_issue", "cand_wait", "winner+gather+scale", "row_wait",
          "z+sync2", "gemv"]
+if os.environ.get("MULTI_NAMES"):
+    NAMES = ["v+argmax+sync", "cand_send", "cluster_wait", "publish", "record_poll+sync", "swap+gather+scale",
+             "row_poll+z+sync", "gemv"]
 lib = _capi.load()
 for case in sys.argv[1:]:
     n, w = (int(v) for v in case.split(":"))
@@ -26,7 +30,7 @@ for case in sys.argv[1:]:
     lib.skl_debug_set_panel_profile(buf.data_ptr()); once(); torch.cuda.synchronize()
     lib.skl_debug_set_panel_profile(None)
     p = buf.view(160, 16).cpu().numpy().astype(float)
-    for c in (0, 7, 15):
+    for c in ((0, 7, 15) if not os.environ.get("MULTI_NAMES") else (0, 50, 100)):
         st = max(p[c, 8], 1)
         print(json.dumps({"n": n, "w": w, "cta": c, "steps": int(st), "sum": round(p[c, :8].sum() / st),
                           **{NAMES[i]: round(p[c, i] / st) for i in range(8)},
