@@ -66,3 +66,9 @@ def test_small_tile_gemm_bit_identical(tmp_path):
     # trailing updates with few 128x128 tiles run on 64x64-tile CTAs (gemm_lower_small_kernel):
     # same DMMA k order per element, one add into C -> bit-identical factors
     same(run(tmp_path, "small", SKL_GEMM_SMALL_TILES=296), run(tmp_path, "big", SKL_GEMM_SMALL_TILES=0))
+
+
+def test_gemm_tail_split_bit_identical(tmp_path):
+    # a partial last wave of 128x128 tiles runs as 64x64 quarters after the full waves
+    pin = dict(SKL_GEMM_SMALL_TILES=0)
+    same(run(tmp_path, "split", SKL_GEMM_TAIL_SPLIT=1, **pin), run(tmp_path, "nosplit", SKL_GEMM_TAIL_SPLIT=0, **pin))
