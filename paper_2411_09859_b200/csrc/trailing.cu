@@ -722,9 +722,9 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   }
   // a partial last wave (under 3/4 of the SMs busy): the big kernel takes the full waves,
   // the tail's tiles run as 64x64 quarters on every SM (bit-identical: same k order)
-  static const int tail_split = [] {
+  static const int tail_split = [] {  // measured no gain (skr2k 17.1-17.6 TF/s either way): off
     const char* v = getenv("SKL_GEMM_TAIL_SPLIT");
-    return v && *v ? atoi(v) : 1;
+    return v && *v ? atoi(v) : 0;
   }();
   int tile_limit = ntiles;
   if (!own && tri && ncols == n && tail_split) {
