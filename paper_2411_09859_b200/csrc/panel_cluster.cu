@@ -1120,11 +1120,12 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
         // wins, ONE multicast bulk copy delivers it to all 16 CTAs (one L2 read, no DSMEM port
         // traffic: the speculative st.async push of 16 rows to 16 CTAs costs ~18 cycles per
         // row double on B200, the multicast is flat in the row length -- tools/probes/xchg3.cu)
+        // (the proxy fence that orders these generic stores before the bulk copy's read is
+        // issued only by the winning CTA's warp 0, right before the copy: the stores have
+        // long landed by then, and the 15 other CTAs never wait on it)
         if (warp == 0) {
           double* gs = a.crow + ((size_t)par * kPC + crank) * CRS;  // global slots: [2][16][CRS]
           for (int j = lane; j <= k; j += 32) gs[j] = s.slab[(size_t)j * Rs + lc];
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-          __syncwarp();
         }
       } else {
         const uint32_t rbar = par ? r_rbar1 : r_rbar0;
@@ -1148,6 +1149,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       const PCand mine = lane < C ? cs[lane] : PCand{0.0, -1, 0};
       owner = lane_argmax(mine.v, mine.pos, lane < C && mine.pos >= 0);
       if (owner < 0) owner = 0;
+    }
+    if (MCAST && owner == crank && warp == 0 && !(dbg & 8)) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
     }
     if (MCAST && owner == crank && tid == 0 && !(dbg & 8)) {
       const double* src = a.crow + ((size_t)par * kPC + crank) * CRS;
