@@ -550,10 +550,15 @@ def main():
         per_launch_bytes = alg_bytes / cnt["panel"]
         per_launch_s = per_fact["panel"] / cnt["panel"] * 1e-3
         ach = per_launch_bytes / per_launch_s / 1e9
+        # the slab stays on chip (DRAM traffic ~0.09x the model bytes), so the step rate is
+        # the figure that moves: eliminations per microsecond of panel time
+        steps = N - 1
         roof = {"kernel": "panel_push_kernel (pivoted left-looking panel, one 16-CTA cluster)", "bound": "hbm",
                 "achieved": round(ach, 2), "peak": hbm_peak, "unit": "GB/s", "frac": round(ach / hbm_peak, 4),
                 "traffic": panel_dram_traffic(), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": int(per_launch_bytes), "launches_per_step": cnt["panel"]}
+                "algorithmic_bytes_per_launch": int(per_launch_bytes), "launches_per_step": cnt["panel"],
+                "eliminations": steps, "us_per_elimination": round(per_fact["panel"] * 1e3 / steps, 4),
+                "eliminations_per_us": round(steps / (per_fact["panel"] * 1e3), 4)}
     gemm_tf = fc.level3 / (per_fact["trailing_gemm"] * 1e-3) / 1e12 if per_fact["trailing_gemm"] else None
 
     # ---- skr2k microbench (config 2b): C(4096^2 lower) += W B^T - B W^T -----------
