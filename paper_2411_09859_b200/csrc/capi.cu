@@ -176,7 +176,7 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
   static int multi_q = env_int("SKL_MULTI_Q", 0);    // cap on the co-resident clusters used
   // cap on the multi-cluster panel width: n=16384 sweep (tools/sweep_multi.sh) 117.8-118.6 ms at 128
   // vs 120.7 ms uncapped (256): the per-step gemv grows with the width faster than the GEMM gains
-  static int multi_nb = env_int("SKL_MULTI_NB", 128);
+  static int multi_nb = env_int("SKL_MULTI_NB", 190);  // round 2 (lean multi-cluster panel): 128/158/190 -> 103.3/101.6/101.4 ms at config 3
   if (Cmax > 0 && multi) {
     for (int csize : {Cmax, 8}) {
       int Q = skl::panel_multi_clusters(csize, smem_limit());
