@@ -145,16 +145,9 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       static int min_w = env_int("SKL_MIN_CLUSTER_W", 64);
       static int ll_single = env_int("SKL_LL_SINGLE", 1);
       const int npush = (ll_single && panel_push()) ? C : 0;  // room for the pushed candidate rows
-      // tall panels (more than SKL_GPU_NB_ROWS rows) use SKL_GPU_NB_TALL columns: the lean
-      // panel kernel register-caches 64 slab columns of a 256-row CTA, wider tall panels
-      // stream the rest from shared memory every step
-      static int nb_tall = env_int("SKL_GPU_NB_TALL", 0);
-      static int tall_rows = env_int("SKL_GPU_NB_ROWS", 2048);
-      // short trailing matrices: ONE panel finishes them (no trailing GEMMs left) when the
-      // whole slab fits the lean panel kernel's shared memory (SKL_FINAL_ROWS)
-      static int final_rows = env_int("SKL_FINAL_ROWS", 0);  // measured slower at 600 (config 1: 1.025 -> 1.076 ms)
-      int cap = (nb_tall > 0 && rows > tall_rows) ? nb_tall : gpu_nb;
-      if (rows <= final_rows) cap = want;
+      // (round 2 measured and dropped: 64-column tall panels and one full-width final panel,
+      // DESIGN.md §4)
+      const int cap = gpu_nb;
       int w = (cap > 0 && want > cap) ? cap : want;
       auto fits = [&](int ww) {
         const int km = r + ww - lo;

@@ -124,7 +124,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
                      const double* __restrict__ Q, int k4cap, int nk4_host,
                      const int* __restrict__ nk4_dev, double* __restrict__ C, long long ldc, int n, double beta,
                      const int* __restrict__ own_tab, long long own_cbase, int own_nbd, int own_g, int own_rank,
-                     int ncols, int tri, int tile_limit) {
+                     int ncols, int tri) {
   // n: C rows; ncols: C columns (== n and tri == 1 except for the tile-table
   // rectangular mode of skew_tridiag_gemm); tri: only row > col is written
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -141,7 +141,7 @@ gemm_lower_nt_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_cons
   // the next tile's MMAs; diagonal tiles keep the masked register epilogue
   const bool bulk_ok = use_tmap && beta == 1.0;
   const int nt = tiles_for(n);
-  const int ntiles = kOwned ? own_tab[1] : min(nt * (nt + 1) / 2, tile_limit);  // tile_limit: see launch_gemm_lower
+  const int ntiles = kOwned ? own_tab[1] : nt * (nt + 1) / 2;
   const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
   const int nchunks = (nk4 + kK4PerStage - 1) / kK4PerStage;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -352,32 +352,21 @@ constexpr int kSmT = 64, kSmThreads = 128, kSmStages = 3, kSmK4 = 4;
 constexpr int kSmHalf = 8 * 32;  // doubles of a half k4 block (8 m8 blocks)
 constexpr size_t kSmSmem = size_t(kSmStages) * 2 * kSmK4 * kSmHalf * sizeof(double) + 2 * kSmStages * 8 + 128;
 
-// tail_base >= 0: the CTAs cover the 128x128 tiles tail_base.. of gemm_lower_nt_kernel's raster
-// (the last, partial wave of a big update), four 64x64 quarters each
 __global__ void __launch_bounds__(kSmThreads) gemm_lower_small_kernel(const double* __restrict__ P,
                                                                       const double* __restrict__ Q, int k4cap,
                                                                       int nk4_host, const int* __restrict__ nk4_dev,
                                                                       double* __restrict__ C, long long ldc, int n,
-                                                                      double beta, int tail_base) {
+                                                                      double beta) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* sP = reinterpret_cast<double*>(smem_raw);
   double* sQ = sP + kSmStages * kSmK4 * kSmHalf;
   uint64_t* full = reinterpret_cast<uint64_t*>(sQ + kSmStages * kSmK4 * kSmHalf);
   const int nk4 = nk4_dev ? *nk4_dev : nk4_host;
-  int ti, tj;
-  if (tail_base >= 0) {
-    int bi, bj;
-    lower_tile_swizzled(tail_base + int(blockIdx.x >> 2), tiles_for(n), bi, bj);
-    ti = 2 * bi + int((blockIdx.x >> 1) & 1);
-    tj = 2 * bj + int(blockIdx.x & 1);
-    if (ti < tj || ti * kSmT >= n) return;  // upper quarter of a diagonal tile / past the edge
-  } else {
-    const int t = blockIdx.x;
-    ti = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-    while (ti * (ti + 1) / 2 > t) --ti;
-    tj = t - ti * (ti + 1) / 2;
-  }
+  const int t = blockIdx.x;
+  int ti = int((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+  while (ti * (ti + 1) / 2 > t) --ti;
+  const int tj = t - ti * (ti + 1) / 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 1, wn = warp & 1;
   const int nch = (nk4 + kSmK4 - 1) / kSmK4;
@@ -717,33 +706,19 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   if (!own && tri && ncols == n && ntiles < small_max) {
     const int nt64 = (n + kSmT - 1) / kSmT;
     gemm_lower_small_kernel<<<nt64 * (nt64 + 1) / 2, kSmThreads, kSmSmem, stream>>>(P, Q, k4cap, nk4, nk4_dev, C,
-                                                                                   ldc, n, beta, -1);
+                                                                                   ldc, n, beta);
     return cudaGetLastError();
   }
-  // a partial last wave (under 3/4 of the SMs busy): the big kernel takes the full waves,
-  // the tail's tiles run as 64x64 quarters on every SM (bit-identical: same k order)
-  static const int tail_split = [] {  // measured no gain (skr2k 17.1-17.6 TF/s either way): off
-    const char* v = getenv("SKL_GEMM_TAIL_SPLIT");
-    return v && *v ? atoi(v) : 0;
-  }();
-  int tile_limit = ntiles;
-  if (!own && tri && ncols == n && tail_split) {
-    const int rem = ntiles % nsm;
-    if (rem > 0 && 4 * rem < 3 * nsm && ntiles > nsm) tile_limit = ntiles - rem;
-  }
-  int grid = tile_limit < nsm ? tile_limit : nsm;
+  // (a split of a partial last wave into 64x64 quarters measured no gain: DESIGN.md §4)
+  int grid = ntiles < nsm ? ntiles : nsm;
   if (own)
     gemm_lower_nt_kernel<true><<<grid, kGemmThreads, kGemmSmem, stream>>>(
         cmap, pmap, use_tmap, P, Q, k4cap, nk4, nk4_dev, C, ldc, n, beta, own->tab, own->cbase, own->nbd, own->G,
-        own->rank, ncols, tri, ntiles);
+        own->rank, ncols, tri);
   else
     gemm_lower_nt_kernel<false><<<grid, kGemmThreads, kGemmSmem, stream>>>(cmap, pmap, use_tmap, P, Q, k4cap, nk4,
                                                                            nk4_dev, C, ldc, n, beta, nullptr, 0, 1,
-                                                                           1, 0, n, 1, tile_limit);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || tile_limit == ntiles) return e;
-  gemm_lower_small_kernel<<<4 * (ntiles - tile_limit), kSmThreads, kSmSmem, stream>>>(P, Q, k4cap, nk4, nk4_dev, C,
-                                                                                      ldc, n, beta, tile_limit);
+                                                                           1, 0, n, 1);
   return cudaGetLastError();
 }
 

@@ -48,7 +48,7 @@ def close(a, b):
 def test_multicast_bit_identical_to_dsmem_push(tmp_path):
     # the DSMEM push reserves 16 row slots in shared memory: pin the GPU panel widths so
     # both runs use the same plan (the factorization is only bit-stable for a fixed plan)
-    pin = dict(SKL_GPU_NB=80, SKL_FINAL_ROWS=0)
+    pin = dict(SKL_GPU_NB=80)
     same(run(tmp_path, "mc", SKL_PUSH_MCAST=1, **pin), run(tmp_path, "dp", SKL_PUSH_MCAST=0, **pin))
 
 
@@ -67,8 +67,3 @@ def test_small_tile_gemm_bit_identical(tmp_path):
     # same DMMA k order per element, one add into C -> bit-identical factors
     same(run(tmp_path, "small", SKL_GEMM_SMALL_TILES=296), run(tmp_path, "big", SKL_GEMM_SMALL_TILES=0))
 
-
-def test_gemm_tail_split_bit_identical(tmp_path):
-    # a partial last wave of 128x128 tiles runs as 64x64 quarters after the full waves
-    pin = dict(SKL_GEMM_SMALL_TILES=0)
-    same(run(tmp_path, "split", SKL_GEMM_TAIL_SPLIT=1, **pin), run(tmp_path, "nosplit", SKL_GEMM_TAIL_SPLIT=0, **pin))
