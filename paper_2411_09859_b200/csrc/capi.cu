@@ -249,6 +249,7 @@ struct BlkWorkspace {
   uint64_t* recs;
   double* crow;
   double* arowg;
+  double* rowmir;
   double* pbuf;
   size_t ll_bytes;
   int k4cap, slot_words, np;
@@ -283,6 +284,7 @@ size_t layout_blk(int n, int nb, const std::vector<PanelPlan>& plan, void* base,
   w.col_group = b.take<int>(n);
   w.disp_list = b.take<int>(2 * (nelim_max + 1));
   w.disp_count = b.take<int>(1);
+  w.rowmir = b.take<double>((size_t)n * (kmax + 4));
   size_t ll_start = align_up(b.off);
   w.slots = b.take<uint64_t>((size_t)ctas * 2 * slot_words);
   w.rowa = b.take<uint64_t>((size_t)2 * slot_words);
@@ -677,6 +679,7 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
     a.rowa = ws.rowa;
     a.recs = ws.recs;
     a.crow = ws.crow;
+    a.rowmir = ws.rowmir;
     a.arowg = ws.arowg;
     a.pbuf = ws.pbuf;
     a.tag0 = tag;
@@ -786,6 +789,7 @@ size_t layout_dist(int n, int nb, int nr, const std::vector<PanelPlan>& plan, vo
   w.col_group = b.take<int>(n);
   w.disp_list = b.take<int>(2 * (nelim_max + 1));
   w.disp_count = b.take<int>(1);
+  w.rowmir = b.take<double>((size_t)n * (kmax + 4));
   size_t ll_start = align_up(b.off);
   w.slots = b.take<uint64_t>((size_t)ctas * 2 * slot_words);
   w.rowa = b.take<uint64_t>((size_t)2 * slot_words);
@@ -924,6 +928,7 @@ int skl_ltlt_blk_piv_dist(int n, int nb, int variant, int nbd, int nranks, int r
       a.rowa = ws.rowa;
       a.recs = ws.recs;
       a.crow = ws.crow;
+      a.rowmir = ws.rowmir;
       a.arowg = ws.arowg;
       a.pbuf = ws.pbuf;
       a.tag0 = tag;

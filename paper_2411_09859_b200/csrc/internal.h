@@ -105,6 +105,7 @@ struct PanelArgs {
   uint64_t* recs;        // LL candidate records [2][P][4]
   double* crow;          // cluster panel: candidate rows [2][C][kmax+2]
   double* arowg;         // cluster panel: row a [2][kmax+2]
+  double* rowmir;        // lean panel: row-major mirror of the slab [rows][push_crs(kmax)] (multicast source)
   double* pbuf;          // multi-cluster panel: slab output [kmax][n]
   uint32_t tag0;         // first LL tag of this panel
   int nblocks;           // CTAs (co-resident)

@@ -962,7 +962,13 @@ __device__ __forceinline__ int lane_argmax(double v, int pos, bool valid) {
 // row are consecutive lanes; they hold the row's state redundantly and split the gemv's
 // columns (j % TPR == part), combining the partial sums with xor-shuffles.  NBANK banks
 // of 32 slab columns are register-cached (each of the TPR threads caches its 32/TPR).
-template <int RPT, int NBANK, int TPR, bool MCAST>
+// MCAST: pivot-row delivery.  0 = every CTA pushes its candidate row to every CTA by
+// st.async; 1 = the winning CTA multicasts its row (written to a global slot during the
+// exchange) once the winner is known; 2 = every CTA multicasts its candidate row straight
+// from the row-major global mirror of the slab (a.rowmir, kept current by the owning
+// threads) at the same time as it sends its candidate, so the rows travel during the
+// candidate exchange and no delivery follows the winner.
+template <int RPT, int NBANK, int TPR, int MCAST>
 __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   static_assert(RPT == 1 || TPR == 1, "either rows per thread or threads per row");
   constexpr int RPB = kPThreads / TPR;   // rows per row-block of the CTA's threads
@@ -970,7 +976,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int crank = int(cg::this_cluster().block_rank());
   const int C = int(cg::this_cluster().num_blocks());  // <= 16
-  constexpr int NSLOT = MCAST ? 1 : kPC;
+  constexpr int NSLOT = MCAST == 1 ? 1 : kPC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int part = TPR > 1 ? (tid & (TPR - 1)) : 0;
   const int rowt = TPR > 1 ? tid / TPR : tid;  // this thread's (first) local row
@@ -995,7 +1001,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   // (pivot row); the last thread arms each barrier for step g + 2 as soon as step g's
   // wait returns, so no arming sits on warp 0's path to the candidate send
   constexpr int kArm = kPThreads - 1;
-  auto row_bytes = [&](int gg) { return (MCAST ? 1u : uint32_t(C)) * 16u * uint32_t((gg - lo + 2) >> 1); };
+  auto row_bytes = [&](int gg) { return (MCAST == 1 ? 1u : uint32_t(C)) * 16u * uint32_t((gg - lo + 2) >> 1); };
   if (tid == kArm) {
     for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);
     fence_mbar_init();
@@ -1010,7 +1016,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   }
 #ifdef SKL_CHECKED
   assert(C >= 1 && C <= kPC && R <= RPT * RPB && kmax <= n && lo >= -1 && r >= lo && rt <= n - 1 + 1);
-  assert(psmem_layout(R, kmax, nullptr, nullptr, MCAST ? 1 : kPC) <= 232448);
+  assert(psmem_layout(R, kmax, nullptr, nullptr, MCAST == 1 ? 1 : kPC) <= 232448);
 #endif
   // per-row state in registers: row li = rowt + u * RPB
   int lab[RPT], ph[RPT];
@@ -1026,7 +1032,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     vv[u] = 0.0;
     cneg[u] = false;
     cn[u] = (li < rcount && pos > r) ? W[(long long)r * ld + pos] : 0.0;
-    if (part == 0 && li < rcount && lo < r) s.slab[li] = W[(long long)lo * ld + pos];  // var2a carry column
+    if (part == 0 && li < rcount && lo < r) {  // var2a carry column
+      const double c0 = W[(long long)lo * ld + pos];
+      s.slab[li] = c0;
+      if (MCAST == 2) a.rowmir[(size_t)(crank * R + li) * CRS] = c0;
+    }
   }
   double rb[RPT][CPB * NBANK];
   int nbank = 0;
@@ -1095,6 +1105,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       if (lane == (wl < 0 ? 0 : wl)) s.wcand[warp] = PWCand{bv, wl < 0 ? -1 : bpos, bph, bli, {0, 0, 0}};
     }
     PMARK(0);
+    // mode 2: this thread's mirror stores of the previous step (long landed) become visible
+    // to the bulk-copy engine before any thread of the CTA can issue this step's multicast
+    if (MCAST == 2) asm volatile("fence.proxy.async.global;" ::: "memory");
     __syncthreads();
     PMARK(1);
     // ---- (2) CTA candidate -> every CTA; its row -> every CTA ---------------
@@ -1115,7 +1128,18 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       // every CTA was measured slower: ~1000 cycles per poll round on B200)
       // this thread -> CTA dst, pairs tid/16 + 16 i
       if (dbg & 8) {
-      } else if (MCAST) {
+      } else if (MCAST == 2) {
+        // the candidate row, contiguous in the global mirror, to slot [par][crank] of every CTA
+        if (tid == 32) {
+          const double* src = a.rowmir + (size_t)(crank * R + lc) * CRS;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, "
+              "[%3], %4;" ::"r"(smem_u32(s.crows + ((size_t)par * kPC + crank) * CRS)),
+              "l"(src), "r"(16u * uint32_t(np)), "r"(smem_u32(&s.xbar[2 + par])),
+              "h"((unsigned short)((1u << C) - 1u))
+              : "memory");
+        }
+      } else if (MCAST == 1) {
         // the candidate row -> this CTA's global slot (warp 0, after the candidate send); if it
         // wins, ONE multicast bulk copy delivers it to all 16 CTAs (one L2 read, no DSMEM port
         // traffic: the speculative st.async push of 16 rows to 16 CTAs costs ~18 cycles per
@@ -1150,11 +1174,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       owner = lane_argmax(mine.v, mine.pos, lane < C && mine.pos >= 0);
       if (owner < 0) owner = 0;
     }
-    if (MCAST && owner == crank && warp == 0 && !(dbg & 8)) {
+    if (MCAST == 1 && owner == crank && warp == 0 && !(dbg & 8)) {
       asm volatile("fence.proxy.async.global;" ::: "memory");
       __syncwarp();
     }
-    if (MCAST && owner == crank && tid == 0 && !(dbg & 8)) {
+    if (MCAST == 1 && owner == crank && tid == 0 && !(dbg & 8)) {
       const double* src = a.crow + ((size_t)par * kPC + crank) * CRS;
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
@@ -1210,7 +1234,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       } else if (lab[u] > a_pos) {
         const double sv = (dbg & 4) ? vv[u] : (vb != 0.0 ? vv[u] / vb : vv[u]);
         vv[u] = sv;
-        if (part == 0) col[rowt + u * RPB] = sv;
+        if (part == 0) {
+          col[rowt + u * RPB] = sv;
+          if (MCAST == 2) a.rowmir[(size_t)(crank * R + rowt + u * RPB) * CRS + k] = sv;
+        }
       }
     }
     PMARK(4);
@@ -1219,7 +1246,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     if (tid == kArm && g + 2 < rt && !(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], row_bytes(g + 2));
     PMARK(5);
     if (more) {
-      const double* xrow = s.crows + ((size_t)par * NSLOT + (MCAST ? 0 : owner)) * CRS;
+      const double* xrow = s.crows + ((size_t)par * NSLOT + (MCAST == 1 ? 0 : owner)) * CRS;
       for (int j = tid; j <= k; j += kPThreads) {
         const double xm = j >= 1 ? xrow[j - 1] : 0.0;
         const double xp = (j + 1 < k) ? xrow[j + 1] : (j + 1 == k ? 1.0 : 0.0);
@@ -1799,7 +1826,7 @@ int panel_multi_clusters(int csize, size_t smem) {
 
 int push_mcast();
 size_t panel_push_smem_bytes(int rows_per, int kmax) {
-  return psmem_layout(rows_per, kmax, nullptr, nullptr, push_mcast() ? 1 : kPC);
+  return psmem_layout(rows_per, kmax, nullptr, nullptr, push_mcast() == 1 ? 1 : kPC);
 }
 
 bool panel_push_v2();
@@ -1823,18 +1850,22 @@ bool panel_push_v2() {
   return on != 0;
 }
 
-// SKL_PUSH_MCAST=0: the speculative DSMEM push of every candidate row (A/B builds)
+// SKL_PUSH_MCAST: 0 = speculative DSMEM push of every candidate row, 1 = winner multicast,
+// 2 = every candidate row multicast from the global row mirror during the exchange
 int push_mcast() {
   static const int mcast = [] {
     const char* v = getenv("SKL_PUSH_MCAST");
-    return v && *v ? atoi(v) : 1;
+    const int m = v && *v ? atoi(v) : 2;
+    return m < 0 || m > 2 ? 2 : m;
   }();
   return mcast;
 }
 
 template <int RPT, int NB, int TPR>
 cudaError_t launch_push_t(const PanelArgs& a, size_t smem, cudaStream_t stream) {
-  auto kern = push_mcast() ? panel_push_kernel<RPT, NB, TPR, true> : panel_push_kernel<RPT, NB, TPR, false>;
+  const int mode = push_mcast();
+  auto kern = mode == 2 ? panel_push_kernel<RPT, NB, TPR, 2>
+                        : (mode == 1 ? panel_push_kernel<RPT, NB, TPR, 1> : panel_push_kernel<RPT, NB, TPR, 0>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
