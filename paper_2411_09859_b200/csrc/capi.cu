@@ -364,6 +364,7 @@ size_t skl_skr2k_workspace_size(int n, int k) {
   b.take<double>(skl::packed_elems(std::max(n, 1), k4cap));
   b.take<int>(std::max(k, 1));
   b.take<int>(4 + std::max(k, 1));
+  b.take<unsigned>(skl::rank2k_prep_scratch_words(k));
   return b.off + 256;
 }
 
@@ -405,9 +406,21 @@ int skl_skr2k_lower(int n, int k, double alpha, const double* A, long long lda, 
     }
     return SKL_OK;
   }
-  g_kt.launches += 3;
-  SKL_TRY(skl::launch_rank2k_keep(A, lda, B, ldb, n, k, skip_zero_cols, keep, cnt, cnt + 1, st));
-  SKL_TRY(skl::launch_pack_rank2k(A, lda, B, ldb, n, k, alpha, keep, cnt, k4cap, P, Q, st));
+  // keep list + packed operands in one cooperative launch (SKL_SKR2K_PREP=0: the
+  // four-launch prologue, kept for A/B), then the lower-triangular DMMA GEMM
+  static const bool fused_prep = [] {
+    const char* v = getenv("SKL_SKR2K_PREP");
+    return !(v && *v == '0');
+  }();
+  if (fused_prep) {
+    unsigned* part = b.take<unsigned>(skl::rank2k_prep_scratch_words(k));
+    g_kt.launches += 2;
+    SKL_TRY(skl::launch_rank2k_prep(A, lda, B, ldb, n, k, skip_zero_cols, alpha, k4cap, part, keep, cnt, P, Q, st));
+  } else {
+    g_kt.launches += 4;
+    SKL_TRY(skl::launch_rank2k_keep(A, lda, B, ldb, n, k, skip_zero_cols, keep, cnt, cnt + 1, st));
+    SKL_TRY(skl::launch_pack_rank2k(A, lda, B, ldb, n, k, alpha, keep, cnt, k4cap, P, Q, st));
+  }
   SKL_TRY(skl::launch_gemm_lower(P, Q, k4cap, k4cap, cnt + 1, C, ldc, n, beta, st));
   if (keff_dev) SKL_TRY(cudaMemcpyAsync(keff_dev, cnt, sizeof(int), cudaMemcpyDeviceToDevice, st));
   return SKL_OK;

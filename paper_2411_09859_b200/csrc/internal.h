@@ -69,6 +69,13 @@ cudaError_t launch_pack_rank2k(const double* A, long long lda, const double* B, 
                                double alpha, const int* keep, const int* keff_dev, int k4cap, double* P,
                                double* Q, cudaStream_t stream);
 
+// the same prologue (keep list + packed operands) in one cooperative launch;
+// part: rank2k_prep_scratch_words(k) words of scratch; cnt[0] = keff, cnt[1] = nk4
+size_t rank2k_prep_scratch_words(int k);
+cudaError_t launch_rank2k_prep(const double* A, long long lda, const double* B, long long ldb, int n, int k,
+                               int skip_zero, double alpha, int k4cap, unsigned* part, int* keep, int* cnt, double* P,
+                               double* Q, cudaStream_t stream);
+
 cudaError_t launch_form_w(const double* A, long long lda, int n, int k, const double* tau, double* W,
                           long long ldw, cudaStream_t stream);
 

@@ -906,7 +906,7 @@ __host__ __device__ inline size_t psmem_layout(int R, int kmax, PSmem* s, unsign
   if (s) s->slab = (double*)p;
   p = take(sizeof(double) * 2 * nslots * (size_t)push_crs(kmax));
   if (s) s->crows = (double*)p;
-  p = take(sizeof(double) * (kmax + 2));
+  p = take(sizeof(double) * (kmax + 10));  // + 8 zeroed spares: gemv_slab_cols reads z in groups of eight
   if (s) s->zbuf = (double*)p;
   p = take(sizeof(double) * (kmax + 2));
   if (s) s->taus = (double*)p;
@@ -956,6 +956,27 @@ __device__ __forceinline__ int lane_argmax(double v, int pos, bool valid) {
   const bool c2 = c1 && lo == m2;
   const unsigned id = __reduce_min_sync(0xffffffffu, c2 ? unsigned(pos) : 0xffffffffu);
   return __ffs(__ballot_sync(0xffffffffu, c2 && unsigned(pos) == id)) - 1;
+}
+
+// A z over the shared-memory slab columns [j0, k) of one row (j0 even): eight column loads
+// issued before the FMAs of a trip, columns >= k predicated off (z beyond k is zero or
+// finite: zbuf carries eight spare zeroed entries), no remainder loop.  Chains by column % 4.
+__device__ __forceinline__ void gemv_slab_cols(const double* __restrict__ sl, int Rs, const double2* __restrict__ z2,
+                                               int j0, int k, double& c0, double& c1, double& c2, double& c3) {
+  for (int j = j0; j < k; j += 8) {
+    double x[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) x[e] = j + e < k ? sl[(size_t)(j + e) * Rs] : 0.0;
+    const double2 za = z2[j >> 1], zb = z2[(j >> 1) + 1], zc = z2[(j >> 1) + 2], zd = z2[(j >> 1) + 3];
+    c0 = fma(x[0], za.x, c0);
+    c1 = fma(x[1], za.y, c1);
+    c2 = fma(x[2], zb.x, c2);
+    c3 = fma(x[3], zb.y, c3);
+    c0 = fma(x[4], zc.x, c0);
+    c1 = fma(x[5], zc.y, c1);
+    c2 = fma(x[6], zd.x, c2);
+    c3 = fma(x[7], zd.y, c3);
+  }
 }
 
 // RPT rows per thread (TPR == 1), or TPR threads per row (RPT == 1): the TPR threads of a
@@ -1010,8 +1031,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       mbar_arrive_expect_tx(&s.xbar[2 + (gg & 1)], row_bytes(gg));
     }
   }
-  for (int j = tid; j < kmax + 2; j += kPThreads) {
-    s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
+  for (int j = tid; j < kmax + 10; j += kPThreads) {
+    if (j < kmax + 2) s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
     s.zbuf[j] = 0.0;
   }
 #ifdef SKL_CHECKED
@@ -1053,6 +1074,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
   cluster_barrier();  // barriers initialised and visible cluster-wide; smem initialised
 #ifdef SKL_PANEL_PROFILE
   long long pp[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long wp[4] = {0, 0, 0, 0};
   long long tp = clock64();
 #define PMARK(i)                \
   do {                          \
@@ -1167,6 +1189,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     mbar_wait_delivered(&s.xbar[par], phase);
     if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[par], uint32_t(C * sizeof(PCand)));
     PMARK(3);
+#ifdef SKL_PANEL_PROFILE
+    const long long wt0 = clock64();
+#endif
     const PCand* cs = s.cand + par * kPC;
     int owner;
     {
@@ -1236,13 +1261,21 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
         vv[u] = sv;
         if (part == 0) {
           col[rowt + u * RPB] = sv;
-          if (MCAST == 2) a.rowmir[(size_t)(crank * R + rowt + u * RPB) * CRS + k] = sv;
+          // dbg 128 (timing only): no mirror store.  (Issuing this store behind the z barrier
+          // instead measured +0.09 ms on config 2.)
+          if (MCAST == 2 && !(dbg & 128)) a.rowmir[(size_t)(crank * R + rowt + u * RPB) * CRS + k] = sv;
         }
       }
     }
     PMARK(4);
+#ifdef SKL_PANEL_PROFILE
+    const long long wt1 = clock64();
+#endif
     // ---- (4) z = T x for the next column (x = pivot row, pushed) -----------
     if (!(dbg & 8)) mbar_wait_delivered(&s.xbar[2 + par], phase);
+#ifdef SKL_PANEL_PROFILE
+    const long long wt2 = clock64();
+#endif
     if (tid == kArm && g + 2 < rt && !(dbg & 8)) mbar_arrive_expect_tx(&s.xbar[2 + par], row_bytes(g + 2));
     PMARK(5);
     if (more) {
@@ -1259,7 +1292,19 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
       s.pivbuf[g - r] = b - a_pos;
       s.taus[k] = vb;
     }
+#ifdef SKL_PANEL_PROFILE
+    const long long wt3 = clock64();
+#endif
     __syncthreads();
+#ifdef SKL_PANEL_PROFILE
+    if (lane == 0) {  // per warp: winner..scale, pivot-row wait, z, wait at the second barrier
+      const long long wt4 = clock64();
+      wp[0] += wt1 - wt0;
+      wp[1] += wt2 - wt1;
+      wp[2] += wt3 - wt2;
+      wp[3] += wt4 - wt3;
+    }
+#endif
     PMARK(6);
     if (!more) break;
     // ---- (5) A z for the next column: kk = k + 1 columns ---------------------
@@ -1311,16 +1356,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
         PSUB(9);
         const double* sl = s.slab + li;
         if constexpr (TPR == 1) {
-          const double2* z2 = reinterpret_cast<const double2*>(s.zbuf);
-          int j = 32 * nbank;
-          for (; j + 3 < k; j += 4) {
-            const double2 za = z2[j >> 1], zb = z2[(j >> 1) + 1];  // j even
-            c0 = fma(sl[(size_t)j * Rs], za.x, c0);
-            c1 = fma(sl[(size_t)(j + 1) * Rs], za.y, c1);
-            c2 = fma(sl[(size_t)(j + 2) * Rs], zb.x, c2);
-            c3 = fma(sl[(size_t)(j + 3) * Rs], zb.y, c3);
-          }
-          for (; j < k; ++j) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
+          gemv_slab_cols(sl, Rs, reinterpret_cast<const double2*>(s.zbuf), 32 * nbank, k, c0, c1, c2, c3);
           c1 = fma(vv[u], zk, c1);  // column k, freshly scaled, from the register
         } else {
           // four predicated column loads per trip, all issued before the FMAs (a short
@@ -1357,6 +1393,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_push_kernel(PanelArgs a) {
     a.prof[crank * 16 + 8] += (unsigned long long)(rt - r);
     for (int i = 8; i < 13; ++i) a.prof[crank * 16 + 1 + i] += (unsigned long long)pp[i];
   }
+  if (a.prof && lane == 0 && crank < 16)  // rows 32..159: per (CTA, warp) sub-phase clocks
+    for (int i = 0; i < 4; ++i) a.prof[(32 + crank * kPWarps + warp) * 16 + i] += (unsigned long long)wp[i];
 #endif
 #undef PMARK
 #undef PSUB
@@ -1446,8 +1484,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
       mbar_arrive_expect_tx(&s.xbar[2 + (gg & 1)], slot_bytes(gg));
     }
   }
-  for (int j = tid; j < kmax + 2; j += kPThreads) {
-    s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
+  for (int j = tid; j < kmax + 10; j += kPThreads) {
+    if (j < kmax + 2) s.taus[j] = (j == 0 && lo >= 0 && lo < n - 1) ? a.tau[lo] : 0.0;
     s.zbuf[j] = 0.0;
   }
   int lab[RPT], ph[RPT];
@@ -1689,15 +1727,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
           }
         }
         const double* sl = s.slab + li;
-        int j = 32 * nbank;
-        for (; j + 3 < k; j += 4) {
-          const double2 za = z2[j >> 1], zb = z2[(j >> 1) + 1];
-          c0 = fma(sl[(size_t)j * Rs], za.x, c0);
-          c1 = fma(sl[(size_t)(j + 1) * Rs], za.y, c1);
-          c2 = fma(sl[(size_t)(j + 2) * Rs], zb.x, c2);
-          c3 = fma(sl[(size_t)(j + 3) * Rs], zb.y, c3);
-        }
-        for (; j < k; ++j) c0 = fma(sl[(size_t)j * Rs], s.zbuf[j], c0);
+        gemv_slab_cols(sl, Rs, z2, 32 * nbank, k, c0, c1, c2, c3);
         c1 = fma(vv[u], zk, c1);
         az[u] = kk >= 2 ? (c0 + c1) + (c2 + c3) : 0.0;
       }

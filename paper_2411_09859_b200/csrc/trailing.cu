@@ -20,6 +20,7 @@
 // written (test_core.py:39-58 NaN-poison invariant).
 #include <algorithm>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -606,6 +607,100 @@ __global__ void pack_rank2k_kernel(const double* __restrict__ A, long long lda, 
   }
 }
 
+// skr2k prologue in ONE cooperative launch (kernels3.py:318-321 + the packing):
+//  phase 1  every CTA scans a block of rows of A and B and records, per column,
+//           "this block holds a nonzero of A / of B" as two bits (plain stores to
+//           its own words of `part`, so nothing needs zeroing);
+//  grid barrier;
+//  phase 2  every CTA ORs the per-block words, builds the ordered keep list in
+//           shared memory (columns nonzero in both factors), CTA 0 publishes keep /
+//           keff / nk4, and all CTAs pack P = alpha [A_keep | B_keep], Q = [B_keep | -A_keep].
+// Replaces memset + flags + compact + pack (four dependent launches, ~30 us of the
+// 120 us config-2b microbench) by one.
+constexpr int kPrepThreads = 1024;
+__global__ void __launch_bounds__(kPrepThreads, 1)
+rank2k_prep_kernel(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb, int n,
+                   int k, int skip_zero, double alpha, int k4cap, unsigned* __restrict__ part, int* __restrict__ keep,
+                   int* __restrict__ cnt, double* __restrict__ P, double* __restrict__ Q) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int words = (k + 15) >> 4;  // two bits per column
+  unsigned* bits = reinterpret_cast<unsigned*>(smem_raw);  // [words]
+  int* skeep = reinterpret_cast<int*>(bits + words);       // [k]
+  __shared__ int s_keff;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = kPrepThreads >> 5;
+  for (int i = tid; i < words; i += kPrepThreads) bits[i] = 0u;
+  __syncthreads();
+  if (skip_zero) {
+    // row blocks of a multiple of 32 rows, one per CTA
+    int rc = (n + gridDim.x - 1) / gridDim.x;
+    rc = (rc + 31) & ~31;
+    const int r0 = blockIdx.x * rc, r1 = min(n, r0 + rc);
+    if (r0 < r1) {
+      for (int j = warp; j < k; j += nw) {
+        int nzA = 0, nzB = 0;
+        for (int i = r0 + lane; i < r1; i += 32) {
+          nzA |= A[(long long)j * lda + i] != 0.0;
+          nzB |= B[(long long)j * ldb + i] != 0.0;
+        }
+        nzA = __any_sync(0xffffffffu, nzA);
+        nzB = __any_sync(0xffffffffu, nzB);
+        if (lane == 0 && (nzA || nzB)) atomicOr(&bits[j >> 4], unsigned((nzA ? 1 : 0) | (nzB ? 2 : 0)) << (2 * (j & 15)));
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < words; i += kPrepThreads) part[(size_t)blockIdx.x * words + i] = bits[i];
+    __threadfence();
+    cooperative_groups::this_grid().sync();
+    for (int i = tid; i < words; i += kPrepThreads) bits[i] = 0u;
+    __syncthreads();
+    const int tot = (int)gridDim.x * words;
+    for (int i = tid; i < tot; i += kPrepThreads) {
+      const unsigned v = __ldcg(part + i);
+      if (v) atomicOr(&bits[i % words], v);
+    }
+    __syncthreads();
+  }
+  if (warp == 0) {
+    int base = 0;
+    for (int j0 = 0; j0 < k; j0 += 32) {
+      const int j = j0 + lane;
+      const bool on = j < k && (!skip_zero || ((bits[j >> 4] >> (2 * (j & 15))) & 3u) == 3u);
+      const unsigned bal = __ballot_sync(0xffffffffu, on);
+      if (on) skeep[base + __popc(bal & ((1u << lane) - 1u))] = j;
+      base += __popc(bal);
+    }
+    if (lane == 0) s_keff = base;
+  }
+  __syncthreads();
+  const int keff = s_keff;
+  if (blockIdx.x == 0) {
+    for (int i = tid; i < keff; i += kPrepThreads) keep[i] = skeep[i];
+    if (tid == 0) {
+      cnt[0] = keff;
+      cnt[1] = (2 * keff + 3) / 4;
+    }
+  }
+  const size_t total = (size_t)tiles_for(n) * kTile * 4 * k4cap;
+  for (size_t off = blockIdx.x * (size_t)kPrepThreads + tid; off < total; off += (size_t)gridDim.x * kPrepThreads) {
+    int row, col;
+    packed_decode(off, k4cap, row, col);
+    double p = 0.0, q = 0.0;
+    if (row < n && col < 2 * keff) {
+      const int j = skeep[col < keff ? col : col - keff];
+      const double av = A[(long long)j * lda + row], bv = B[(long long)j * ldb + row];
+      if (col < keff) {
+        p = alpha * av;
+        q = bv;
+      } else {
+        p = alpha * bv;
+        q = -av;
+      }
+    }
+    P[off] = p;
+    Q[off] = q;
+  }
+}
+
 // W = A S with T = S - S^T (core.py:153-169, kernels3.py:354-364):
 // even columns zero; odd j: W[:, j] = -tau[j-1] A[:, j-1] + tau[j] A[:, j+1] (second term if j+1 < k)
 __global__ void form_w_kernel(const double* __restrict__ A, long long lda, int n, int k,
@@ -818,6 +913,32 @@ cudaError_t launch_pack_rank2k(const double* A, long long lda, const double* B, 
   pack_rank2k_kernel<<<grid_for(total, 256), 256, 0, stream>>>(A, lda, B, ldb, n, alpha, keep, keff_dev, k4cap, P,
                                                                Q);
   return cudaGetLastError();
+}
+
+size_t rank2k_prep_scratch_words(int k) {
+  // one (k + 15) / 16-word bit row per CTA of the cooperative grid (at most one CTA per SM; 256 bounds the SM count)
+  return (size_t)256 * (size_t)((std::max(k, 1) + 15) / 16);
+}
+
+cudaError_t launch_rank2k_prep(const double* A, long long lda, const double* B, long long ldb, int n, int k,
+                               int skip_zero, double alpha, int k4cap, unsigned* part, int* keep, int* cnt, double* P,
+                               double* Q, cudaStream_t stream) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = sizeof(unsigned) * (size_t)((k + 15) / 16) + sizeof(int) * (size_t)std::max(k, 1);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 40 * 1024) {
+    cudaError_t e =
+        cudaFuncSetAttribute(rank2k_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  int grid = std::min(nsm, 256);
+  void* args[] = {&A, &lda, &B, &ldb, &n, &k, &skip_zero, &alpha, &k4cap, &part, &keep, &cnt, &P, &Q};
+  return cudaLaunchCooperativeKernel((void*)rank2k_prep_kernel, dim3(grid), dim3(kPrepThreads), args, smem, stream);
 }
 
 cudaError_t launch_form_w(const double* A, long long lda, int n, int k, const double* tau, double* W,

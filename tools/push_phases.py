@@ -36,3 +36,8 @@ for case in sys.argv[1:]:
                           **{NAMES[i]: round(p[c, i] / st) for i in range(8)},
                           "gemv_sub(zk,cached,uncached)": [round(p[c, 9 + i] / st) for i in range(3)],
                           "p1_sub(armed,v_done)": [round(p[c, 12 + i] / st) for i in range(2)]}))
+    if not os.environ.get("MULTI_NAMES"):
+        for c in (0, 7, 15):
+            st = max(p[c, 8], 1)
+            print(f"  n={n} cta {c} per warp [winner..scale, row_wait, z, sync2_wait]: " +
+                  " ".join("w%d:%s" % (w, [round(p[32 + c * 8 + w, i] / st) for i in range(4)]) for w in range(8)))
