@@ -910,13 +910,13 @@ __host__ __device__ inline size_t psmem_layout(int R, int kmax, PSmem* s, unsign
   if (s) s->zbuf = (double*)p;
   p = take(sizeof(double) * (kmax + 2));
   if (s) s->taus = (double*)p;
-  p = take(sizeof(PCand) * 2 * kPC);
+  p = take(sizeof(PCand) * (2 * kPC + 4));  // + [2][2]: the global winner's record (multi-cluster panel)
   if (s) s->cand = (PCand*)p;
   p = take(sizeof(PWCand) * kPWarps);
   if (s) s->wcand = (PWCand*)p;
   p = take(sizeof(int) * (kmax + 2));
   if (s) s->pivbuf = (int*)p;
-  p = take(sizeof(uint64_t) * 4);
+  p = take(sizeof(uint64_t) * 6);  // [4 + par]: winner record (multi-cluster panel)
   if (s) s->xbar = (uint64_t*)p;
   return off;
 }
@@ -1477,11 +1477,12 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
   constexpr int kArm = kPThreads - 1;
   auto slot_bytes = [&](int gg) { return uint32_t(sizeof(uint64_t)) * uint32_t(6 + 2 * (gg - lo + 1)); };
   if (tid == kArm) {
-    for (int i = 0; i < 4; ++i) mbar_init(&s.xbar[i], 1);
+    for (int i = 0; i < 6; ++i) mbar_init(&s.xbar[i], 1);
     fence_mbar_init();
     for (int gg = r; gg < rt && gg < r + 2; ++gg) {
       mbar_arrive_expect_tx(&s.xbar[gg & 1], uint32_t(C * sizeof(PCand)));
       mbar_arrive_expect_tx(&s.xbar[2 + (gg & 1)], slot_bytes(gg));
+      mbar_arrive_expect_tx(&s.xbar[4 + (gg & 1)], uint32_t(2 * sizeof(PCand)));
     }
   }
   for (int j = tid; j < kmax + 10; j += kPThreads) {
@@ -1509,6 +1510,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
   const uint32_t r_cand = mapa_u32(smem_u32(s.cand), lanec);
   const uint32_t r_cbar0 = mapa_u32(smem_u32(&s.xbar[0]), lanec);
   const uint32_t r_cbar1 = mapa_u32(smem_u32(&s.xbar[1]), lanec);
+  const uint32_t r_wbar0 = mapa_u32(smem_u32(&s.xbar[4]), lanec);
+  const uint32_t r_wbar1 = mapa_u32(smem_u32(&s.xbar[5]), lanec);
   cluster_barrier();
 #ifdef SKL_PANEL_PROFILE
   long long pp[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1602,6 +1605,21 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
         rec = PCand{__longlong_as_double((long long)((uint64_t(vhi) << 32) | vlo)), int(pp), int(pph)};
       }
       const int gl = lane_argmax(rec.v, rec.pos, lane < Q && rec.pos >= 0);
+      // the winning record straight to the CTAs of this cluster by st.async (it is what the
+      // interchange, the gathers and the scaling wait for); the row follows by the multicast
+      // and is only needed for z
+      {
+        const int src = gl < 0 ? 0 : gl;
+        const unsigned long long vw = (unsigned long long)__double_as_longlong(__shfl_sync(0xffffffffu, rec.v, src));
+        const int posw = __shfl_sync(0xffffffffu, rec.pos, src);
+        const int phw = __shfl_sync(0xffffffffu, rec.ph, src);
+        if (lane < C) {
+          const uint32_t rdst = r_cand + uint32_t((2 * kPC + 2 * par) * sizeof(PCand));
+          const uint32_t rbar = par ? r_wbar1 : r_wbar0;
+          st_async_v4(rdst, rbar, uint32_t(vw), uint32_t(vw >> 32), uint32_t(posw), uint32_t(phw));
+          st_async_v4(rdst + uint32_t(sizeof(PCand)), rbar, uint32_t(src), 0u, 0u, 0u);
+        }
+      }
       if (lane == 0) {
         const uint64_t* src = a.slots + ((size_t)(gl < 0 ? 0 : gl) * 2 + par) * a.slot_words;
         asm volatile(
@@ -1612,36 +1630,15 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
       }
     }
     QMARK(3);
-    mbar_wait_delivered(&s.xbar[2 + par], phase);
-    if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[2 + par], slot_bytes(g + 2));
+    mbar_wait_delivered(&s.xbar[4 + par], phase);
+    if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[4 + par], uint32_t(2 * sizeof(PCand)));
     const uint64_t* ms = mslot + (size_t)par * SW;
     PCand w;
     int wq;
     {
-      uint64_t w0 = ms[0], w1 = ms[1], w2 = ms[2], w3 = ms[3], w4 = ms[4];
-      if (uint32_t(w0 >> 32) != tag || uint32_t(w1 >> 32) != tag || uint32_t(w2 >> 32) != tag ||
-          uint32_t(w3 >> 32) != tag || uint32_t(w4 >> 32) != tag) {
-        // the copy raced the publication (never seen): read the record through L2; the
-        // winning cluster is the one whose record the leader saw, i.e. any valid best
-        PCand best{0.0, -1, 0};
-        int bq = 0;
-        for (int q = 0; q < Q; ++q) {
-          const uint64_t* slot = a.slots + ((size_t)q * 2 + par) * a.slot_words;
-          uint32_t vlo, vhi, pp, pph;
-          ll_get4(slot, tag, vlo, vhi, pp, pph);
-          const PCand c{__longlong_as_double((long long)((uint64_t(vhi) << 32) | vlo)), int(pp), int(pph)};
-          if (c.pos >= 0 && (best.pos < 0 || fabs(c.v) > fabs(best.v) || (fabs(c.v) == fabs(best.v) && c.pos < best.pos))) {
-            best = c;
-            bq = q;
-          }
-        }
-        w = best;
-        wq = bq;
-      } else {
-        w = PCand{__longlong_as_double((long long)((uint64_t(uint32_t(w1)) << 32) | uint32_t(w0))), int(uint32_t(w2)),
-                  int(uint32_t(w3))};
-        wq = int(uint32_t(w4));
-      }
+      const PCand* ws2 = s.cand + 2 * kPC + 2 * par;
+      w = ws2[0];
+      wq = *reinterpret_cast<const int*>(ws2 + 1);
     }
     QMARK(4);
     const int a_pos = g + 1, b = w.pos, pb = w.ph;
@@ -1667,6 +1664,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
     }
     QMARK(5);
     // ---- (5) z = T x (x = the winning row, from the multicast copy) ----------------
+    mbar_wait_delivered(&s.xbar[2 + par], phase);
+    if (tid == kArm && g + 2 < rt) mbar_arrive_expect_tx(&s.xbar[2 + par], slot_bytes(g + 2));
     if (more) {
       const uint64_t* xs = ms + 6;
       const uint64_t* xr = a.slots + ((size_t)wq * 2 + par) * a.slot_words + 6;
