@@ -54,6 +54,42 @@ def test_skew_rank2k_config2_microbench_shape():
     assert np.max(np.abs(got[low] - want[low])) <= 1e-13 * k * np.max(np.abs(want[low]))
 
 
+@pytest.mark.parametrize("n,k", [(5, 3), (33, 17), (1200, 40), (600, 600)])
+def test_skew_rank2k_keep_list_edge_cases(n, k):
+    """The one-launch prologue (flag bits per row block, grid barrier, ordered keep list) against
+    kernels3.py:318-321: a column is kept only if it is nonzero in BOTH factors, wherever the
+    nonzero sits (first row, last row, a row block of its own), with or without the skipping."""
+    a = RNG.standard_normal((n, k))
+    b = RNG.standard_normal((n, k))
+    a[:, 0] = 0.0                      # zero in A only
+    b[:, k - 1] = 0.0                  # zero in B only
+    if k > 4:
+        a[:, 2] = 0.0
+        a[n - 1, 2] = 3.0              # a single nonzero, in the last row
+        b[:, 3] = 0.0
+        b[0, 3] = -2.0                 # a single nonzero, in the first row
+        a[:, 4] = 0.0
+        b[:, 4] = 0.0                  # zero in both
+    for skip in (True, False):
+        c = np.asfortranarray(RNG.standard_normal((n, n)))
+        want = c.copy()
+        keff = oracle.skew_rank2k(want, 0.75, a, b, skip_zero_columns=skip)
+        got = c.copy()
+        k3().skew_rank2k(got, 0.75, a, b, 1.0, skip_zero_columns=skip)
+        low = np.tril(np.ones((n, n), bool), -1)
+        assert k3().last_keff == keff
+        assert np.allclose(got[low], want[low], rtol=1e-12, atol=1e-12 * k)
+        assert np.array_equal(got[~low], c[~low])
+    # nothing survives: C is only scaled
+    z = np.zeros((n, k))
+    c = np.asfortranarray(RNG.standard_normal((n, n)))
+    got = c.copy()
+    k3().skew_rank2k(got, 1.0, z, b, 2.0)
+    assert k3().last_keff == 0
+    low = np.tril(np.ones((n, n), bool), -1)
+    assert np.array_equal(got[low], 2.0 * c[low]) and np.array_equal(got[~low], c[~low])
+
+
 def test_skew_rank2k_alias_and_shape_errors():
     a = RNG.standard_normal((6, 6))
     with pytest.raises(ValueError):
