@@ -706,6 +706,15 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
     a.pivot = pivot;
     a.info = info;
     a.push = (p.cluster == 2 && p.ctas == p.csize && pivot && panel_push()) ? 1 : 0;
+    const int ntr = n - rt;
+    // cluster panels followed by a trailing update: epilogue + operand packing as ONE
+    // cooperative launch (SKL_FUSED_FINISH=0: finish_gather, finish_write, pack_rankk)
+    // (worth ~12 us per panel while the three kernels are launch-bound: config 1 0.868 -> 0.842 ms,
+    // config 2 8.56 -> 8.50 ms; from ~8K trailing rows on the separate, wider grids win: config 3
+    // 100.6 -> 101.2 ms with every panel fused, hence the row limit)
+    static const int fused_rows = env_int("SKL_FUSED_FINISH", 8192);
+    const bool fuse = ntr < fused_rows && p.cluster != 0 && ntr >= 2 && !left;
+    a.defer_finish = fuse ? 1 : 0;
     {
       KScope ks(KPANEL, st);
       if (p.cluster == 2)
@@ -714,11 +723,10 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
         SKL_TRY(skl::launch_panel_cluster(a, st));
       else
         SKL_TRY(skl::launch_panel(a, st));
-      if (p.cluster != 0) g_kt.launches += 2;  // + panel_finish_gather / panel_finish_write
+      if (p.cluster != 0 && !fuse) g_kt.launches += 2;  // + panel_finish_gather / panel_finish_write
     }
     tag += (uint32_t)p.nelim + 1;
 
-    const int ntr = n - rt;
     if (ntr >= 2 && !left) {
       const int ka = rt - p.lo;
       const int K = ka + (straggler ? 2 : 0);
@@ -726,8 +734,13 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
       const int sh0 = skl::align_shift(rt, ld), rt0 = rt - sh0;
       {
         KScope ks(KPACK, st);
-        SKL_TRY(skl::launch_pack_rankk(ws.W + (size_t)p.lo * ld + rt, ld, ntr, ka, tau + p.lo + 1, -1.0,
-                                       straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st, sh0));
+        if (fuse) {
+          skl::FinishPack f{ntr, ka, ws.k4cap, sh0, tau + p.lo + 1, straggler ? ws.y + rt : nullptr, ws.P, ws.Q};
+          SKL_TRY(skl::launch_panel_finish_pack(a, f, st));
+        } else {
+          SKL_TRY(skl::launch_pack_rankk(ws.W + (size_t)p.lo * ld + rt, ld, ntr, ka, tau + p.lo + 1, -1.0,
+                                         straggler ? ws.y + rt : nullptr, ws.k4cap, ws.P, ws.Q, st, sh0));
+        }
       }
       {
         // the C region starts sh0 rows/columns early (zero operand rows there) so

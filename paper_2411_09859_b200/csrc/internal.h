@@ -124,6 +124,7 @@ struct PanelArgs {
   int pivot;             // 0: unpivoted (pivot row = row g+1), exact-zero breakdown -> *info
   int* info;             // device: first breaking column + 1 (0 = none); may be null when pivot
   int push;              // single-cluster pivoted panel: candidate rows pushed by st.async, lazy interchanges
+  int defer_finish;      // 1: the launcher leaves the finish kernels to launch_panel_finish_pack()
 };
 size_t panel_smem_bytes(int rows_per, int kmax);
 int panel_max_ctas();
@@ -139,6 +140,18 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream);
 // multi-cluster variant (cooperative; intra-cluster DSMEM + inter-cluster LL exchange)
 int panel_multi_clusters(int csize, size_t smem);
 cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t stream);
+// Panel epilogue and operand packing in ONE cooperative launch (a.defer_finish = 1 panels):
+// displaced trailing lines -> side buffer and P / Q packed straight from the panel buffer,
+// grid barrier, panel buffer -> L columns and side -> trailing lines.  Same results as
+// launch_panel_finish + launch_pack_rankk (three launches of ~6 us each per panel).
+struct FinishPack {
+  int rows, ka, k4cap, shift;  // trailing rows, panel columns, packed k4 capacity, alignment shift
+  const double* t;             // tau of the panel columns (ka - 1 couplings)
+  const double* y;             // var1 straggler vector (position indexed from rt) or null
+  double* P;
+  double* Q;
+};
+cudaError_t launch_panel_finish_pack(const PanelArgs& a, const FinishPack& f, cudaStream_t stream);
 
 // packed factor layout (core.py:349-375)
 cudaError_t launch_pack_factor(int n, const double* L, long long ldl, const double* tau, double* X, long long ldx,

@@ -16,6 +16,7 @@
 // narrows the panel when it would not fit (the factorization is invariant to
 // the GPU block width; pivots stay those of the reference).
 #include <cooperative_groups.h>
+#include <algorithm>
 #include <cassert>
 
 #include "common.cuh"
@@ -841,6 +842,91 @@ cudaError_t launch_panel_finish(const PanelArgs& a, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+
+// The panel epilogue and the packing of the trailing update's operands as one cooperative
+// kernel.  Phase A reads only: the displaced trailing lines go to the side buffer (they must
+// see the pre-panel W), and P = -A, Q = A T^T (+ the var1 straggler pair) are packed
+// straight from the panel buffer (by position, rows >= rt) -- the same values finish_write
+// is about to copy into W's columns [lo, rt).  Grid barrier.  Phase B writes W: panel
+// buffer -> L columns, side buffer -> trailing lines.  Three dependent ~6 us launches per
+// panel become one.
+__device__ __forceinline__ size_t fp_packed_elems(int rows, int k4cap) {
+  return (size_t)tiles_for(rows) * kTile * 4 * k4cap;
+}
+__global__ void __launch_bounds__(256) panel_finish_pack_kernel(PanelArgs a, FinishPack f) {
+  const int n = a.n, lo = a.lo, rt = a.r + a.nelim, ntr = n - rt, row0 = lo + 1;
+  const long long ld = a.ld;
+  const int nd = *a.disp_count;
+  const int GX = min(16, max(1, (ntr + 255) / 256));  // row chunks of a line, as in the two-launch epilogue
+  const int nb = int(gridDim.x);
+  // ---- A1: displaced trailing lines -> side buffer
+  for (int w = blockIdx.x; w < nd * GX; w += nb) {
+    const int q = w / GX, bx = w - q * GX;
+    const int p = a.disp_list[q];
+    const int pp = a.gperm[p];
+    double* line = a.side + (size_t)q * ntr;
+    for (int i = rt + bx * 256 + threadIdx.x; i < n; i += GX * 256)
+      line[i - rt] = (i == p) ? 0.0 : skew_at(a.W, a.ld, a.gperm[i], pp);
+  }
+  // ---- A2: packed operands from the panel buffer (pack_rankk_kernel, trailing.cu)
+  if (f.rows > 0) {
+    const double* A = a.pbuf + rt;  // A[row, col] = pbuf[col * n + rt + row]
+    const size_t total = fp_packed_elems(f.rows + f.shift, f.k4cap);
+    for (size_t off = blockIdx.x * (size_t)256 + threadIdx.x; off < total; off += (size_t)nb * 256) {
+      const int lane = int(off & 31), mb = int((off >> 5) & 15);
+      const size_t rest = off >> 9;
+      const int qk = int(rest % (size_t)f.k4cap), tl = int(rest / (size_t)f.k4cap);
+      const int row = tl * kTile + mb * 8 + (lane >> 2) - f.shift;
+      const int col = qk * 4 + (lane & 3);
+      double pv = 0.0, qv = 0.0;
+      if (row >= 0 && row < f.rows) {
+        if (col < f.ka) {
+          const double* ar = A + row;
+          pv = -1.0 * ar[(size_t)col * n];
+          double acc = 0.0;
+          if (col >= 1) acc = f.t[col - 1] * ar[(size_t)(col - 1) * n];
+          if (col + 1 < f.ka) acc -= f.t[col] * ar[(size_t)(col + 1) * n];
+          qv = acc;
+        } else if (f.y != nullptr && row >= 1 && col < f.ka + 2) {
+          const double lv = A[(size_t)(f.ka - 1) * n + row];
+          const double yv = f.y[row];
+          if (col == f.ka) {
+            pv = lv;
+            qv = yv;
+          } else {
+            pv = -yv;
+            qv = lv;
+          }
+        }
+      }
+      f.P[off] = pv;
+      f.Q[off] = qv;
+    }
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  // ---- B1: panel buffer -> L columns [lo, rt)
+  const int GY = a.kmax;
+  for (int w = blockIdx.x; w < GY * GX; w += nb) {
+    const int j = w / GX, bx = w - j * GX;
+    const int c = lo + j;
+    for (int pos = max(row0, c + 1) + bx * 256 + threadIdx.x; pos < n; pos += GX * 256)
+      a.W[(long long)c * ld + pos] = a.pbuf[(size_t)j * n + pos];
+  }
+  // ---- B2: side buffer -> trailing lines
+  for (int w = blockIdx.x; w < nd * GX; w += nb) {
+    const int q = w / GX, bx = w - q * GX;
+    const int p = a.disp_list[q];
+    const double* line = a.side + (size_t)q * ntr;
+    for (int i = rt + bx * 256 + threadIdx.x; i < n; i += GX * 256) {
+      const double v = line[i - rt];
+      if (i > p)
+        a.W[(long long)p * ld + i] = v;
+      else if (i < p)
+        a.W[(long long)i * ld + p] = -v;
+    }
+  }
+}
 
 // ===========================================================================
 // panel_push_kernel: the single-cluster pivoted panel, rebuilt for the shortest
@@ -1767,6 +1853,28 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_multi2_kernel(PanelArgs a)
 
 }  // namespace
 
+cudaError_t launch_panel_finish_pack(const PanelArgs& a, const FinishPack& f, cudaStream_t stream) {
+  static int maxgrid = 0;
+  if (!maxgrid) {
+    int dev = 0, nsm = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, panel_finish_pack_kernel, 256, 0) != cudaSuccess || per < 1)
+      per = 1;
+    maxgrid = nsm * (per > 4 ? 4 : per);
+  }
+  // enough CTAs for the largest phase (256 elements each), at most the co-resident grid
+  const int ntr = a.n - (a.r + a.nelim);
+  const size_t pk = f.rows > 0 ? (size_t)tiles_for(f.rows + f.shift) * kTile * 4 * f.k4cap : 0;
+  const size_t wr = (size_t)a.kmax * (size_t)(ntr > 0 ? ntr : 1);
+  size_t want = (std::max(pk, wr) + 255) / 256;
+  int grid = (int)std::min<size_t>(std::max<size_t>(want, 1), (size_t)maxgrid);
+  PanelArgs ac = a;
+  FinishPack fc = f;
+  void* args[] = {&ac, &fc};
+  return cudaLaunchCooperativeKernel((void*)panel_finish_pack_kernel, dim3(grid), dim3(256), args, 0, stream);
+}
+
 size_t panel_cluster_smem_bytes(int rows_per, int kmax, int npush) {
   return csmem_layout(rows_per, kmax, nullptr, nullptr, npush);
 }
@@ -1823,7 +1931,7 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream) {
   cfg.numAttrs = 1;
   e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel<false>, a);
   if (e != cudaSuccess) return e;
-  return launch_panel_finish(a, stream);
+  return a.defer_finish ? cudaSuccess : launch_panel_finish(a, stream);
 }
 
 // Largest number of co-resident clusters of size `csize` for a given smem size (0: none).
@@ -1936,7 +2044,7 @@ cudaError_t launch_panel_push(const PanelArgs& a, cudaStream_t stream) {
   else
     e = launch_push_t<1, 2, 8>(a, smem, stream);
   if (e != cudaSuccess) return e;
-  return launch_panel_finish(a, stream);
+  return a.defer_finish ? cudaSuccess : launch_panel_finish(a, stream);
 }
 
 size_t panel_multi2_smem_bytes(int rows_per, int kmax) { return psmem_layout(rows_per, kmax, nullptr, nullptr, 3); }
@@ -1986,7 +2094,7 @@ cudaError_t launch_panel_multi2(const PanelArgs& a, int csize, cudaStream_t stre
   e = a.rows_per > kPThreads ? launch_multi2_t<2, 1>(a, csize, smem, stream)
                              : launch_multi2_t<1, 2>(a, csize, smem, stream);
   if (e != cudaSuccess) return e;
-  return launch_panel_finish(a, stream);
+  return a.defer_finish ? cudaSuccess : launch_panel_finish(a, stream);
 }
 
 // a.nblocks = total CTAs (Q clusters x a.csize); cooperative so all clusters are co-resident
@@ -2019,7 +2127,7 @@ cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t strea
   cfg.numAttrs = a.nblocks > csize ? 2 : 1;
   e = cudaLaunchKernelEx(&cfg, panel_cluster_kernel<true>, a);
   if (e != cudaSuccess) return e;
-  return launch_panel_finish(a, stream);
+  return a.defer_finish ? cudaSuccess : launch_panel_finish(a, stream);
 }
 
 }  // namespace skl
