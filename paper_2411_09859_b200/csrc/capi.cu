@@ -654,6 +654,7 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
   SKL_TRY(cudaMemcpyAsync(ws.col_group, group.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
 
   uint32_t tag = 1;
+  bool count_zeroed = false;  // disp_count left at zero by the previous panel's fused epilogue
   for (int k = 0; k < (int)plan.size(); ++k) {
     const PanelPlan& p = plan[k];
     const int rt = p.r + p.nelim;
@@ -715,6 +716,8 @@ int blk_driver(int n, int nb, int variant, int pivot, int ncols, const double* X
     static const int fused_rows = env_int("SKL_FUSED_FINISH", 8192);
     const bool fuse = ntr < fused_rows && p.cluster != 0 && ntr >= 2 && !left;
     a.defer_finish = fuse ? 1 : 0;
+    a.count_zeroed = count_zeroed ? 1 : 0;
+    count_zeroed = fuse;  // the fused epilogue leaves disp_count at zero
     {
       KScope ks(KPANEL, st);
       if (p.cluster == 2)

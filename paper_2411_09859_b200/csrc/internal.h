@@ -125,6 +125,7 @@ struct PanelArgs {
   int* info;             // device: first breaking column + 1 (0 = none); may be null when pivot
   int push;              // single-cluster pivoted panel: candidate rows pushed by st.async, lazy interchanges
   int defer_finish;      // 1: the launcher leaves the finish kernels to launch_panel_finish_pack()
+  int count_zeroed;      // 1: disp_count is already zero (the previous panel's fused epilogue reset it)
 };
 size_t panel_smem_bytes(int rows_per, int kmax);
 int panel_max_ctas();

@@ -926,6 +926,9 @@ __global__ void __launch_bounds__(256) panel_finish_pack_kernel(PanelArgs a, Fin
         a.W[(long long)i * ld + p] = -v;
     }
   }
+  // every thread read the count at kernel entry: reset it for the next panel (its launcher
+  // then skips the memset)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.disp_count = 0;
 }
 
 // ===========================================================================
@@ -1915,7 +1918,7 @@ cudaError_t launch_panel_cluster(const PanelArgs& a, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(panel_cluster_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  e = a.count_zeroed ? cudaSuccess : cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
@@ -2026,7 +2029,7 @@ cudaError_t launch_push_t(const PanelArgs& a, size_t smem, cudaStream_t stream) 
 // threads per row grow as the rows per CTA shrink (SKL_PUSH_TPR caps it, 1 = off)
 cudaError_t launch_panel_push(const PanelArgs& a, cudaStream_t stream) {
   const size_t smem = panel_push_smem_bytes(a.rows_per, a.kmax);
-  cudaError_t e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  cudaError_t e = a.count_zeroed ? cudaSuccess : cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   static const int tpr_cap = [] {
     const char* v = getenv("SKL_PUSH_TPR");
@@ -2089,7 +2092,7 @@ cudaError_t launch_multi2_t(const PanelArgs& a, int csize, size_t smem, cudaStre
 
 cudaError_t launch_panel_multi2(const PanelArgs& a, int csize, cudaStream_t stream) {
   const size_t smem = panel_multi2_smem_bytes(a.rows_per, a.kmax);
-  cudaError_t e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  cudaError_t e = a.count_zeroed ? cudaSuccess : cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   e = a.rows_per > kPThreads ? launch_multi2_t<2, 1>(a, csize, smem, stream)
                              : launch_multi2_t<1, 2>(a, csize, smem, stream);
@@ -2107,7 +2110,7 @@ cudaError_t launch_panel_multi(const PanelArgs& a, int csize, cudaStream_t strea
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(panel_cluster_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
+  e = a.count_zeroed ? cudaSuccess : cudaMemsetAsync(a.disp_count, 0, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.nblocks);
