@@ -85,16 +85,18 @@ template <typename T>
 struct PhysS {
   T* sm;  // packed columns [J0, n-1) in shared memory
   T* gs;  // packed columns [0, J0) in the CTA's global scratch
-  int n, J0;
-  long long offJ0;
+  const int* coff;  // [n] offset of column q's pointer inside its region (shared memory table:
+                    // the 64-bit packed-offset arithmetic was 20 % of the kernel's stall samples)
+  int J0;
   // pointer such that col(q)[p] = S[p][q] for p > q
-  __device__ __forceinline__ T* col(int q) const {
-    const long long o = pk_off(n, q) - (q + 1);
-    return q >= J0 ? sm + (o - offJ0) : gs + o;
+  __device__ __forceinline__ T* col(int q) const { return (q >= J0 ? sm : gs) + coff[q]; }
+  __device__ __forceinline__ T at(int p, int q) const {
+    const int hi = max(p, q), lo = min(p, q);
+    const T v = col(lo)[hi];
+    return p > q ? v : -v;
   }
-  __device__ __forceinline__ T at(int p, int q) const { return p > q ? col(q)[p] : -col(p)[q]; }
   // storage slot of the pair {p, q} (p != q), no sign
-  __device__ __forceinline__ T* slot(int p, int q) const { return p > q ? col(q) + p : col(p) + q; }
+  __device__ __forceinline__ T* slot(int p, int q) const { return col(min(p, q)) + max(p, q); }
 };
 
 __device__ __forceinline__ int bwarp_argmax(double av, int idx, bool valid) {
@@ -256,13 +258,22 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
   BCand* red = reinterpret_cast<BCand*>(smem_raw);         // [2][kBW]
   int* ibuf = reinterpret_cast<int*>(red + 2 * kBW);       // [0..1] pa slots, [2..2+kBW) warp counts
   int* actl = ibuf + 2 + 2 * kBW;                                   // [n] compact active list / final label map
-  T** cptr = reinterpret_cast<T**>(smem_raw + ((sizeof(BCand) * 2 * kBW + sizeof(int) * (2 + 2 * kBW + n) + 15) & ~size_t(15)));
+  int* coff = actl + n;                                             // [n] column pointer offsets
+  T** cptr = reinterpret_cast<T**>(smem_raw + ((sizeof(BCand) * 2 * kBW + sizeof(int) * (2 + 2 * kBW + 2 * n) + 15) & ~size_t(15)));
   double* taus = reinterpret_cast<double*>(cptr + n);      // [n] tau (Pfaffian factors)
   double* pfred = taus + n;                                // [kBW] log|Pf| partials
   T* pend = reinterpret_cast<T*>(pfred + kBW);             // [n][PS]
   T* smS = pend + (size_t)n * PS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  PhysS<T> S{smS, scr + (long long)blockIdx.x * scr_stride, n, J0, pk_off(n, J0)};
+  {
+    const int offJ0 = int(pk_off(n, J0));
+    for (int q = tid; q < n; q += kBT) {
+      const int o = int(pk_off(n, q)) - (q + 1);
+      coff[q] = q >= J0 ? o - offJ0 : o;
+    }
+  }
+  PhysS<T> S{smS, scr + (long long)blockIdx.x * scr_stride, coff, J0};
+  __syncthreads();
 
 #ifdef SKL_BATCHED_PROF
   long long bpt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -530,7 +541,7 @@ batched_kernel(int batch, int n, int J0, const T* __restrict__ X, long long ldx,
 
 template <typename T>
 size_t batched_head(int n) {
-  size_t h = (sizeof(BCand) * 2 * kBW + sizeof(int) * (2 + 2 * kBW + n) + 15) & ~size_t(15);
+  size_t h = (sizeof(BCand) * 2 * kBW + sizeof(int) * (2 + 2 * kBW + 2 * n) + 15) & ~size_t(15);
   return h + sizeof(T*) * (size_t)n + sizeof(double) * (size_t)(n + kBW) + sizeof(T) * (size_t)n * pend_stride<T>();
 }
 
