@@ -636,15 +636,31 @@ rank2k_prep_kernel(const double* __restrict__ A, long long lda, const double* __
     rc = (rc + 31) & ~31;
     const int r0 = blockIdx.x * rc, r1 = min(n, r0 + rc);
     if (r0 < r1) {
-      for (int j = warp; j < k; j += nw) {
-        int nzA = 0, nzB = 0;
+      // four columns per warp and trip: the eight loads of a row group are issued before
+      // any of them is reduced (one column at a time waited out a DRAM latency per column)
+      for (int j0 = warp; j0 < k; j0 += 4 * nw) {
+        int nzA[4] = {0, 0, 0, 0}, nzB[4] = {0, 0, 0, 0};
         for (int i = r0 + lane; i < r1; i += 32) {
-          nzA |= A[(long long)j * lda + i] != 0.0;
-          nzB |= B[(long long)j * ldb + i] != 0.0;
+          double av[4], bv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = j0 + e * nw;
+            av[e] = j < k ? A[(long long)j * lda + i] : 0.0;
+            bv[e] = j < k ? B[(long long)j * ldb + i] : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            nzA[e] |= av[e] != 0.0;
+            nzB[e] |= bv[e] != 0.0;
+          }
         }
-        nzA = __any_sync(0xffffffffu, nzA);
-        nzB = __any_sync(0xffffffffu, nzB);
-        if (lane == 0 && (nzA || nzB)) atomicOr(&bits[j >> 4], unsigned((nzA ? 1 : 0) | (nzB ? 2 : 0)) << (2 * (j & 15)));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = j0 + e * nw;
+          const int a1 = __any_sync(0xffffffffu, nzA[e]), b1 = __any_sync(0xffffffffu, nzB[e]);
+          if (lane == 0 && j < k && (a1 || b1))
+            atomicOr(&bits[j >> 4], unsigned((a1 ? 1 : 0) | (b1 ? 2 : 0)) << (2 * (j & 15)));
+        }
       }
     }
     __syncthreads();
@@ -681,23 +697,30 @@ rank2k_prep_kernel(const double* __restrict__ A, long long lda, const double* __
     }
   }
   const size_t total = (size_t)tiles_for(n) * kTile * 4 * k4cap;
-  for (size_t off = blockIdx.x * (size_t)kPrepThreads + tid; off < total; off += (size_t)gridDim.x * kPrepThreads) {
-    int row, col;
-    packed_decode(off, k4cap, row, col);
-    double p = 0.0, q = 0.0;
-    if (row < n && col < 2 * keff) {
-      const int j = skeep[col < keff ? col : col - keff];
-      const double av = A[(long long)j * lda + row], bv = B[(long long)j * ldb + row];
-      if (col < keff) {
-        p = alpha * av;
-        q = bv;
-      } else {
-        p = alpha * bv;
-        q = -av;
+  const size_t stride = (size_t)gridDim.x * kPrepThreads;
+  for (size_t off0 = blockIdx.x * (size_t)kPrepThreads + tid; off0 < total; off0 += 4 * stride) {
+    // four packed entries per trip, their loads issued together
+    double av[4], bv[4];
+    bool lowh[4], on[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const size_t off = off0 + e * stride;
+      int row = 0, col = 0;
+      if (off < total) packed_decode(off, k4cap, row, col);
+      on[e] = off < total && row < n && col < 2 * keff;
+      lowh[e] = col < keff;
+      const int j = on[e] ? skeep[lowh[e] ? col : col - keff] : 0;
+      av[e] = on[e] ? A[(long long)j * lda + row] : 0.0;
+      bv[e] = on[e] ? B[(long long)j * ldb + row] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const size_t off = off0 + e * stride;
+      if (off < total) {
+        P[off] = on[e] ? (lowh[e] ? alpha * av[e] : alpha * bv[e]) : 0.0;
+        Q[off] = on[e] ? (lowh[e] ? bv[e] : -av[e]) : 0.0;
       }
     }
-    P[off] = p;
-    Q[off] = q;
   }
 }
 
