@@ -809,10 +809,10 @@ cudaError_t launch_gemm_lower(const double* P, const double* Q, int k4cap, int n
   int nt = tiles_for(n);
   int ntiles = own ? own->ntiles : nt * (nt + 1) / 2;
   if (ntiles == 0) return cudaSuccess;
-  // few 128x128 tiles (under two waves): 64x64 tiles, one 4-warp CTA each (bit-identical)
+  // few 128x128 tiles (under ~four waves): 64x64 tiles, one 4-warp CTA each (bit-identical)
   static const int small_max = [] {
     const char* v = getenv("SKL_GEMM_SMALL_TILES");
-    return v && *v ? atoi(v) : 2 * 148;
+    return v && *v ? atoi(v) : 600;  // ~4 waves of 128x128 tiles (config 2: 1.40 -> 1.34 ms against 296)
   }();
   static bool sattr = false;
   if (!sattr) {
