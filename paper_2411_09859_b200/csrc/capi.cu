@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "internal.h"
 #include "skewltl_b200.h"
@@ -31,12 +33,25 @@ struct KTimer {
   long long launches = 0;
 } g_kt;
 
+// NVTX ranges over the same scopes (SKL_NVTX=1): the host-side phase names of a timeline --
+// the counterpart of the reference's scope("panel") / scope("update") tagging
+// (instrument.py:74-94, blocked.py:92,331,347).  Header-only NVTX v3: no library to link.
+const char* const kScopeName[] = {"skl.panel", "skl.pack", "skl.trailing_gemm", "skl.finalize"};
+bool nvtx_on() {
+  static const bool on = [] {
+    const char* v = getenv("SKL_NVTX");
+    return v && *v && *v != '0';
+  }();
+  return on;
+}
+
 struct KScope {
   int kind;
   cudaStream_t st;
   cudaEvent_t b = nullptr, e = nullptr;
   KScope(int k, cudaStream_t s) : kind(k), st(s) {
     g_kt.launches++;
+    if (nvtx_on()) nvtxRangePushA(kScopeName[kind]);
     if (g_kt.on) {
       cudaEventCreate(&b);
       cudaEventCreate(&e);
@@ -48,6 +63,7 @@ struct KScope {
       cudaEventRecord(e, st);
       g_kt.ev[kind].push_back({b, e});
     }
+    if (nvtx_on()) nvtxRangePop();
   }
 };
 
