@@ -4,7 +4,7 @@
   driver, entered through ``skl_ltlt_unb_twostep``.  From n = 128 up it runs
   the blocked GPU driver (lean cluster panel ``panel_push_kernel`` + DMMA
   trailing update), which computes the same L, T and pivots and is faster
-  (config 1, n=512: 0.99 ms vs 2.9 ms for the fused right-looking kernel);
+  (config 1, n=512: 0.83 ms vs 2.9 ms for the fused right-looking kernel);
   below n = 128 the fused single-cluster two-step kernel (``twostep.cu``:
   eliminations, interchanges, fold and skew rank-2 of each pair in one
   launch) serves it.  DESIGN.md §1 records the decision.
