@@ -67,3 +67,16 @@ def test_small_tile_gemm_bit_identical(tmp_path):
     # same DMMA k order per element, one add into C -> bit-identical factors
     same(run(tmp_path, "small", SKL_GEMM_SMALL_TILES=296), run(tmp_path, "big", SKL_GEMM_SMALL_TILES=0))
 
+
+
+def test_fused_epilogue_bit_identical_to_separate_launches(tmp_path):
+    # panel_finish_pack_kernel packs P / Q straight from the panel buffer and writes the same
+    # W entries as finish_gather + finish_write + pack_rankk: the whole factorization must not
+    # change by a bit (SKL_FUSED_FINISH=0 keeps the three launches)
+    same(run(tmp_path, "fz"), run(tmp_path, "f0", SKL_FUSED_FINISH=0))
+
+
+def test_small_tile_gemm_bit_identical_to_large_tiles(tmp_path):
+    # the 64x64-tile trailing GEMM accumulates every element in the same k order as the
+    # 128x128-tile kernel (the driver switches between them by size)
+    same(run(tmp_path, "gs", SKL_GEMM_SMALL_TILES=100000), run(tmp_path, "gl", SKL_GEMM_SMALL_TILES=0))
