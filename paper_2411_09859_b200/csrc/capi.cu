@@ -163,7 +163,11 @@ bool plan_panel(int n, int r, int want, int lo, int nsm, PanelPlan& p) {
       const int npush = (ll_single && panel_push()) ? C : 0;  // room for the pushed candidate rows
       // (round 2 measured and dropped: 64-column tall panels and one full-width final panel,
       // DESIGN.md §4)
-      const int cap = gpu_nb;
+      // short trailing matrices take wider panels (fewer panel / GEMM launches; the per-step
+      // gemv is cheap at few rows per CTA): SKL_GPU_NB_SHORT columns from SKL_SHORT_ROWS rows down
+      static int short_rows = env_int("SKL_SHORT_ROWS", 600);
+      static int gpu_nb_short = env_int("SKL_GPU_NB_SHORT", 142);  // K = 144: nine 16-wide k-chunks
+      const int cap = (short_rows > 0 && rows <= short_rows && gpu_nb_short > gpu_nb) ? gpu_nb_short : gpu_nb;
       int w = (cap > 0 && want > cap) ? cap : want;
       auto fits = [&](int ww) {
         const int km = r + ww - lo;
