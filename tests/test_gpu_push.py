@@ -73,7 +73,7 @@ def test_fused_epilogue_bit_identical_to_separate_launches(tmp_path):
     # panel_finish_pack_kernel packs P / Q straight from the panel buffer and writes the same
     # W entries as finish_gather + finish_write + pack_rankk: the whole factorization must not
     # change by a bit (SKL_FUSED_FINISH=0 keeps the three launches)
-    same(run(tmp_path, "fz"), run(tmp_path, "f0", SKL_FUSED_FINISH=0))
+    same(run(tmp_path, "fz", SKL_TEST_BIG=1), run(tmp_path, "f0", SKL_FUSED_FINISH=0, SKL_TEST_BIG=1))
 
 
 def test_small_tile_gemm_bit_identical_to_large_tiles(tmp_path):
