@@ -11,6 +11,7 @@
 // a single thread in the reference's operation order (no FMA contraction),
 // then applied to every right-hand side in parallel (back substitution by the
 // reciprocal pivots).
+#include <cooperative_groups.h>
 #include <cfloat>
 #include <map>
 #include <mutex>
@@ -234,6 +235,147 @@ __global__ void __launch_bounds__(256) trsm_fused_kernel(int n, const double* __
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) zin[i] -= acc;
     }
+  }
+}
+
+// The whole triangular sweep of 1-2 right-hand sides as ONE cooperative kernel: the loop over
+// the 64-column blocks of trsm_fused_kernel with a grid barrier between blocks instead of a
+// launch per block (n = 4096: 64 + 64 launches of 12-18 us each).  Per block every CTA stages
+// the diagonal block, warp 0 solves it with register shuffles (two entries per lane, the same
+// operations in the same order as the barrier-per-step loop of trsm_fused_kernel), CTA 0
+// writes the solved block to the other buffer and every CTA updates its share of the
+// remaining rows of zin.  A block's solve reads rows the previous block's updates wrote,
+// hence the barrier; the solved block itself is never read again.  Bit-identical results.
+template <bool TRANS>
+__global__ void __launch_bounds__(256) trsm_sweep_kernel(int n, const double* __restrict__ L, long long ld,
+                                                         double* __restrict__ zin_all, long long ldi,
+                                                         double* __restrict__ zout_all, long long ldo) {
+  // lbuf[2][col][row] = L[j0+row, j0+col] of the current and the NEXT block (L is constant: the
+  // next diagonal block is staged while this block's rows are updated, off the critical path)
+  extern __shared__ __align__(16) unsigned char sweep_smem[];
+  typedef double LB[kSolveBlk][kSolveBlk + 1];
+  LB* lbuf = reinterpret_cast<LB*>(sweep_smem);
+  double* zb = reinterpret_cast<double*>(lbuf + 2);
+  static_assert(kSolveBlk == 64, "two entries per lane");
+  const int c = blockIdx.y;
+  double* zin = zin_all + (long long)c * ldi;
+  double* zout = zout_all + (long long)c * ldo;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nblk = (n + kSolveBlk - 1) / kSolveBlk;
+  // the strictly-lower part of diagonal block bi: 16 entries per thread, loaded in one go
+  // (stage_load) and stored to shared memory later (stage_store), so the loads of the next
+  // block fly while this block's rows are updated
+  constexpr int kPerThread = kSolveBlk * kSolveBlk / 256;
+  double sv[kPerThread];
+  auto stage_load = [&](int bi) {
+    const int j0 = bi * kSolveBlk, w = min(n, j0 + kSolveBlk) - j0;
+#pragma unroll
+    for (int e = 0; e < kPerThread; ++e) {
+      const int idx = threadIdx.x + e * 256, cc = idx >> 6, rr = idx & 63;
+      sv[e] = (cc < w && rr > cc && rr < w && j0 + cc >= 1) ? L[(long long)(j0 + cc - 1) * ld + j0 + rr] : 0.0;
+    }
+  };
+  auto stage_store = [&](LB& lb) {
+#pragma unroll
+    for (int e = 0; e < kPerThread; ++e) {
+      const int idx = threadIdx.x + e * 256;
+      lb[idx >> 6][idx & 63] = sv[e];
+    }
+  };
+  stage_load(TRANS ? nblk - 1 : 0);
+  stage_store(lbuf[0]);
+  for (int bi0 = 0; bi0 < nblk; ++bi0) {
+    const int bi = TRANS ? nblk - 1 - bi0 : bi0;
+    const int j0 = bi * kSolveBlk, j1 = min(n, j0 + kSolveBlk);
+    const int w = j1 - j0;
+    LB& lb = lbuf[bi0 & 1];
+    for (int t = threadIdx.x; t < w; t += blockDim.x) zb[t] = __ldcg(zin + j0 + t);
+    // the L entries of this CTA's first pass over the rows to update do not depend on the
+    // block's solution: load them now, so their latency hides behind warp 0's serial solve
+    double lv[16];
+    const int q = threadIdx.x & 3;
+    const int ipre = TRANS ? blockIdx.x * nw + warp : j1 + blockIdx.x * 64 + (threadIdx.x >> 2);
+    if (!TRANS) {
+      if (w == kSolveBlk && ipre < n) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) lv[e] = l_at(L, ld, ipre, j0 + q + 4 * e);
+      }
+    } else {
+      lv[0] = lv[1] = 0.0;
+      if (ipre >= 1 && ipre < j0) {
+        const double* col = L + (long long)(ipre - 1) * ld + j0;
+        lv[0] = lane < w ? col[lane] : 0.0;
+        lv[1] = lane + 32 < w ? col[lane + 32] : 0.0;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double z0 = lane < w ? zb[lane] : 0.0, z1 = lane + 32 < w ? zb[lane + 32] : 0.0;
+      if (!TRANS) {
+        for (int jj = 0; jj < w; ++jj) {
+          const double y = jj < 32 ? __shfl_sync(0xffffffffu, z0, jj) : __shfl_sync(0xffffffffu, z1, jj - 32);
+          if (lane > jj) z0 -= lb[jj][lane] * y;
+          if (lane + 32 > jj && lane + 32 < w) z1 -= lb[jj][lane + 32] * y;
+        }
+      } else {
+        for (int jj = w - 1; jj >= 0; --jj) {
+          const double y = jj < 32 ? __shfl_sync(0xffffffffu, z0, jj) : __shfl_sync(0xffffffffu, z1, jj - 32);
+          if (lane < jj) z0 -= lb[lane][jj] * y;
+          if (lane + 32 < jj) z1 -= lb[lane + 32][jj] * y;
+        }
+      }
+      if (lane < w) zb[lane] = z0;
+      if (lane + 32 < w) zb[lane + 32] = z1;
+    }
+    __syncthreads();
+    if (bi0 + 1 < nblk) stage_load(TRANS ? bi - 1 : bi + 1);
+    if (blockIdx.x == 0)
+      for (int t = threadIdx.x; t < w; t += blockDim.x) zout[j0 + t] = zb[t];
+    if (!TRANS) {
+      // rows below the block: four consecutive lanes per row, lane q takes the columns
+      // t = q (mod 4) -- the four accumulation chains of the thread-per-row update, one per
+      // lane, all 16 loads of a lane in flight at once -- combined as (a0 + a1) + (a2 + a3)
+      for (int i0 = j1 + blockIdx.x * 64; i0 < n; i0 += gridDim.x * 64) {
+        const int i = i0 + (threadIdx.x >> 2);
+        double a = 0.0;
+        if (i < n) {
+          if (w == kSolveBlk) {
+            if (i != ipre) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) lv[e] = l_at(L, ld, i, j0 + q + 4 * e);
+            }
+#pragma unroll
+            for (int e = 0; e < 16; ++e) a = fma(lv[e], zb[q + 4 * e], a);
+          } else {
+            // a partial last block keeps the thread-per-row order: chain 0 takes every column
+            if (q == 0)
+              for (int t = 0; t < w; ++t) a = fma(l_at(L, ld, i, j0 + t), zb[t], a);
+          }
+        }
+        a += __shfl_xor_sync(0xffffffffu, a, 1);
+        a += __shfl_xor_sync(0xffffffffu, a, 2);
+        if (q == 0 && i < n) zin[i] = __ldcg(zin + i) - a;
+      }
+    } else {
+      for (int i = blockIdx.x * nw + warp; i < j0; i += gridDim.x * nw) {
+        double acc = 0.0;
+        if (i >= 1) {
+          double v0 = lv[0], v1 = lv[1];
+          if (i != ipre) {
+            const double* col = L + (long long)(i - 1) * ld + j0;
+            v0 = lane < w ? col[lane] : 0.0;
+            v1 = lane + 32 < w ? col[lane + 32] : 0.0;
+          }
+          acc = fma(v0, lane < w ? zb[lane] : 0.0, v1 * (lane + 32 < w ? zb[lane + 32] : 0.0));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) zin[i] = __ldcg(zin + i) - acc;
+      }
+    }
+    if (bi0 + 1 < nblk) stage_store(lbuf[(bi0 + 1) & 1]);
+    __threadfence();
+    cooperative_groups::this_grid().sync();
   }
 }
 
@@ -518,8 +660,32 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
     return !(v && *v == '0');
   }();
   const bool fused = fused_on && nrhs <= 2;
+  // 1-2 right-hand sides: each triangular sweep as one cooperative kernel (SKL_SOLVE_SWEEP=0: a
+  // fused launch per 64-column block)
+  static const bool sweep_on = [] {
+    const char* v = getenv("SKL_SOLVE_SWEEP");
+    return !(v && *v == '0');
+  }();
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool sweep = fused && sweep_on;
+  auto launch_sweep = [&](bool trans, double* zin, long long ldi, double* zout, long long ldo) {
+    const int work = trans ? (n + 7) / 8 : (n + 63) / 64;  // warp per row / four lanes per row
+    dim3 grid(std::max(1, std::min(work, 2 * nsm / nrhs)), nrhs);
+    void* args[] = {&n, &L, &ldl, &zin, &ldi, &zout, &ldo};
+    const size_t smem = sizeof(double) * (2 * kSolveBlk * (kSolveBlk + 1) + kSolveBlk);
+    void* kern = trans ? (void*)trsm_sweep_kernel<true> : (void*)trsm_sweep_kernel<false>;
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    return cudaLaunchCooperativeKernel(kern, grid, dim3(256), args, smem, stream);
+  };
+  if (sweep && (err = launch_sweep(false, Z, ldz, B, ldb)) != cudaSuccess) return err;
   // L z = P b (forward, blocks of 64 columns); fused: the solved z lands in B
-  for (int j0 = 0; j0 < n; j0 += kSolveBlk) {
+  for (int j0 = 0; j0 < n && !sweep; j0 += kSolveBlk) {
     const int j1 = std::min(n, j0 + kSolveBlk);
     const int rows = n - j1;
     if (fused) {
@@ -539,7 +705,8 @@ cudaError_t launch_solve(int n, int nrhs, const double* L, long long ldl, const 
   tridiag_apply_kernel<<<nrhs, 128, 0, stream>>>(n, nrhs, d, e, f2, mult, swp, info, Zt, ldt);
   // L^T y = z (backward); fused: the solved y lands back in Z
   const int nblk = (n + kSolveBlk - 1) / kSolveBlk;
-  for (int bi = nblk - 1; bi >= 0; --bi) {
+  if (sweep && (err = launch_sweep(true, B, ldb, Z, ldz)) != cudaSuccess) return err;
+  for (int bi = nblk - 1; bi >= 0 && !sweep; --bi) {
     const int j0 = bi * kSolveBlk, j1 = std::min(n, j0 + kSolveBlk);
     if (fused) {
       dim3 grid(std::max(1, std::min((j0 + 7) / 8, 148 * 4)), nrhs);
